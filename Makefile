@@ -1,0 +1,37 @@
+# Builds the product library (sm_100a CUDA kernels + C-ABI host runtime) in-tree:
+#   paper_2211_14969_b200/_lib/libhps_leaf_b200.so
+# and the CPU oracle (test infrastructure) via oracle/Makefile.
+NVCC      ?= nvcc
+ARCH      := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-ffp-contract=off -Iinclude \
+             -Ipaper_2211_14969_b200/csrc -Xptxas -v
+SRC       := paper_2211_14969_b200/csrc
+OBJDIR    := build/obj
+LIB       := paper_2211_14969_b200/_lib/libhps_leaf_b200.so
+CU        := $(SRC)/k1_assemble.cu $(SRC)/k2_lu_schur.cu $(SRC)/k4_scatter.cu $(SRC)/k5_leaf_solve.cu
+CPP       := $(SRC)/hps_host.cpp $(SRC)/hps_api.cpp
+HDRS      := $(wildcard $(SRC)/*.h $(SRC)/*.cuh include/*.h include/hps/*.hpp)
+OBJS      := $(patsubst $(SRC)/%,$(OBJDIR)/%.o,$(CU) $(CPP))
+
+all: $(LIB) oracle
+
+$(OBJDIR)/%.cu.o: $(SRC)/%.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ > $(OBJDIR)/$*.ptxas.log 2>&1 || (cat $(OBJDIR)/$*.ptxas.log; exit 1)
+
+$(OBJDIR)/%.cpp.o: $(SRC)/%.cpp $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -x cu -c $< -o $@
+
+$(LIB): $(OBJS)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+
+oracle:
+	$(MAKE) -s -C oracle
+
+clean:
+	rm -rf build $(LIB)
+	$(MAKE) -s -C oracle clean
+
+.PHONY: all oracle clean

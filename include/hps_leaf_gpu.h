@@ -1,0 +1,138 @@
+/* ===========================================================================
+ * hps_leaf_gpu.h — C-ABI of the B200 HPS leaf stage (libhps_leaf_b200.so).
+ *
+ * The reference (arXiv 2211.14969, /root/reference) specifies the leaf stage as
+ * C++ operations in namespace hps with exceptions
+ * from proj/include/hps/errors.hpp and batching from proj/include/hps/parallel.hpp.
+ * It has no compiled implementation, so this C-ABI is the boundary its own FFI
+ * would bind for the path; each entry point names the reference operation it
+ * replaces.  include/hps/leaf_gpu.hpp is the SPEC-shaped C++ layer over it.
+ *
+ * Conventions
+ *   - No exceptions cross this boundary.  Return codes:
+ *       HPS_OK 0, HPS_ERR_RESONANCE 1 (see status[]), HPS_ERR_PARAM 2,
+ *       HPS_ERR_CUDA 3.  hps_gpu_last_error(ctx) returns the message.
+ *   - Ownership: the library owns device memory and streams; the caller owns
+ *     every host buffer (pinned memory from hps_host_alloc gives overlap).
+ *   - Threading: one ctx per GPU, driven by one host thread; calls on distinct
+ *     ctxs are concurrent-safe; one ctx is not reentrant (parallel.hpp's
+ *     per-worker scratch rule).
+ *   - Layouts (leaf-major, element e = ey*nx + ex; local node l = iy*p + ix;
+ *     boundary order S,E,N,W with corners owned by the first listing edge,
+ *     SPEC.md:314):  b, f, u : p*p per leaf ; T : n_b*n_b row-major per leaf ;
+ *     w, v : n_b per leaf ; S_solve : n_i*n_b row-major per leaf.
+ *     n_i = (p-2)^2, n_b = 4(p-1).
+ *   - Results are bitwise-independent of chunking, leaf range and GPU count
+ *     (parallel.hpp:21-22).
+ * =========================================================================== */
+#ifndef HPS_LEAF_GPU_H
+#define HPS_LEAF_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HPS_OK 0
+#define HPS_ERR_RESONANCE 1
+#define HPS_ERR_PARAM 2
+#define HPS_ERR_CUDA 3
+
+/* SPEC.md:313 storage policy for leaf factors. */
+#define HPS_STORAGE_RECOMPUTE 0
+#define HPS_STORAGE_STORE 1
+
+typedef struct hps_gpu_ctx hps_gpu_ctx;
+
+/* Leaf-stage descriptor: the (p, a, kappa) of build_leaf_operator
+ * (SPEC.md:270-273, 62-70), the element grid of MeshParams,
+ * the storage policy and the device budget for in-flight leaves. */
+typedef struct {
+  int32_t p;               /* nodes per leaf side, 4 <= p <= 45 */
+  int32_t nx, ny;          /* leaf grid (elements) */
+  int32_t storage;         /* HPS_STORAGE_RECOMPUTE (default) or HPS_STORAGE_STORE */
+  double a;                /* leaf side length, > 0 */
+  double kappa;            /* wavenumber, >= 0 */
+  int64_t workspace_bytes; /* 0: 70% of free device memory */
+} hps_leaf_desc;
+
+typedef struct {
+  int32_t p, n_i, n_b, n_leaves;
+  int32_t chunk_leaves;    /* leaves per device chunk */
+  int32_t resident_ctas;   /* leaves in flight per wave (2 per SM) */
+  int64_t workspace_bytes_per_leaf;
+  int64_t n_active;        /* reduced-system unknowns */
+  int64_t N;               /* global DOF */
+} hps_gpu_info_t;
+
+/* Device-side timing of the last call, CUDA events on the compute stream. */
+typedef struct {
+  float ms_total;          /* first kernel start -> last kernel end */
+  float ms_assemble;       /* K1, summed over chunks */
+  float ms_lu_schur;       /* K2+K3, summed over chunks */
+  float ms_scatter;        /* K4 */
+  int32_t kernels;         /* kernels launched by the call */
+  int32_t chunks;
+} hps_gpu_timing_t;
+
+/* Create a context on `device` (hps_gpu_ctx holds streams, tables, workspace). */
+int hps_gpu_create(int device, const hps_leaf_desc* desc, hps_gpu_ctx** out);
+void hps_gpu_destroy(hps_gpu_ctx* ctx);
+const char* hps_gpu_last_error(const hps_gpu_ctx* ctx);
+int hps_gpu_get_info(const hps_gpu_ctx* ctx, hps_gpu_info_t* out);
+int hps_gpu_get_timing(const hps_gpu_ctx* ctx, hps_gpu_timing_t* out);
+
+/* batched_condense (per leaf condense_leaf :279-287) for
+ * elements [e0, e1).  Inputs b, f are the (e1-e0) leaves' samples (host).
+ * Outputs (host, caller-owned): T (T_flux), w (w_equiv), S (S_solve, nullable),
+ * status (0 ok / 1 resonance).  Returns HPS_ERR_RESONANCE if any leaf failed;
+ * the message names the smallest failing element id and all failing ids. */
+int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, const double* f,
+                     double* T, double* w, double* S, int32_t* status);
+
+/* Same operation on device-resident buffers (inputs already in HBM, outputs
+ * stay in HBM), enqueued on `stream` (cudaStream_t, NULL = ctx stream). */
+int hps_gpu_condense_device(hps_gpu_ctx* ctx, int32_t e0, int32_t n, const double* d_b,
+                            const double* d_f, double* d_T, double* d_w, int32_t* d_status,
+                            void* stream);
+
+/* Batched leaf_solve for elements [e0, e1): u = p*p local
+ * values, interior = A_ii^{-1}(f_i - A_ib v), boundary = v.  Recompute policy
+ * rebuilds and refactors A_ii; store policy reuses the
+ * factors kept by the last hps_gpu_condense over the same elements
+ * (bitwise-identical results). */
+int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, const double* f,
+                       const double* v, double* u, int32_t* status);
+
+/* assemble_reduced — K4.  Pattern: CSR of the reduced system
+ * over active nodes, int64 row_ptr (n_active+1), int32 col_idx
+ * (nnz).  Call with row_ptr == NULL to get nnz only. */
+int hps_gpu_reduced_pattern(hps_gpu_ctx* ctx, int64_t* nnz, int64_t* row_ptr, int32_t* col_idx);
+/* Values/rhs from all leaves' T and w (host, leaf-major, all nx*ny leaves) and
+ * Dirichlet samples g_bnd = [south(Nx) | north(Nx) | west(Ny) | east(Ny)],
+ * Nx = nx(p-1)+1, Ny = ny(p-1)+1. */
+int hps_gpu_assemble_reduced(hps_gpu_ctx* ctx, const double* T, const double* w,
+                             const double* g_bnd, double* values, double* rhs);
+/* Device-resident variant (T, w, g_bnd, values, rhs in HBM). */
+int hps_gpu_assemble_reduced_device(hps_gpu_ctx* ctx, const double* d_T, const double* d_w,
+                                    const double* d_g_bnd, double* d_values, double* d_rhs,
+                                    void* stream);
+
+/* Test hook: zero interior row 0 of A_ii for these element
+ * ids, which forces a zero pivot.  n = 0 clears. */
+int hps_gpu_set_fault_injection(hps_gpu_ctx* ctx, const int32_t* elements, int32_t n);
+
+/* Pinned host memory helpers. */
+void* hps_host_alloc(size_t bytes);
+void hps_host_free(void* ptr);
+
+/* Library identity (for load checks). */
+const char* hps_gpu_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HPS_LEAF_GPU_H */

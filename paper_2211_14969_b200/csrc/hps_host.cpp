@@ -1,0 +1,740 @@
+// ============================================================================
+//  hps_host.cpp — host runtime behind the C-ABI (include/hps_leaf_gpu.h).
+//
+//  Replaces the reference's CPU batching (proj/include/hps/parallel.hpp:25-58:
+//  one std::thread worker per leaf) with one context per GPU that streams leaf
+//  chunks through HBM:  H2D(b, f) -> K1 assemble -> K2/K3 LU+Schur -> D2H(T, w)
+//  on three streams with double-buffered I/O, so copies overlap the FP64 work.
+//  Chunk size is derived from the device budget (180 GB HBM on B200) and is a
+//  multiple of the resident-CTA count (2 leaves per SM) so waves stay full.
+//  Results never depend on chunking: every leaf is computed by one CTA with a
+//  schedule that depends on p only.
+// ============================================================================
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "hps_kernels.h"
+#include "hps_leaf_gpu.h"
+
+using hpsg::LeafDims;
+
+namespace {
+
+constexpr int kMaxP = 45;
+
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() { release(); }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+  cudaError_t ensure(size_t n) {
+    if (n <= bytes) return cudaSuccess;
+    release();
+    cudaError_t e = cudaMalloc(&ptr, n);
+    if (e == cudaSuccess) bytes = n;
+    return e;
+  }
+  template <class T> T* as() const { return static_cast<T*>(ptr); }
+};
+
+// ---- 1-D Chebyshev primitives -------
+// Same formulas and summation order as the CPU oracle (bit-identical tables).
+void cheb_tables(int p, double a, std::vector<double>& Ds, std::vector<double>& D2) {
+  std::vector<double> x(p);
+  const double den = 2.0 * double(p - 1);
+  for (int k = 0; k < p; ++k) x[k] = std::sin(M_PI * double(2 * k - (p - 1)) / den);
+  std::vector<double> D(size_t(p) * p, 0.0);
+  for (int i = 0; i < p; ++i) {
+    const double ci = (i == 0 || i == p - 1) ? 2.0 : 1.0;
+    double s = 0.0;
+    for (int j = 0; j < p; ++j) {
+      if (j == i) continue;
+      const double cj = (j == 0 || j == p - 1) ? 2.0 : 1.0;
+      const double sgn = ((i + j) & 1) ? -1.0 : 1.0;
+      const double v = (ci / cj) * sgn / (x[i] - x[j]);
+      D[size_t(i) * p + j] = v;
+      s += v;
+    }
+    D[size_t(i) * p + i] = -s;
+  }
+  const double sc = 2.0 / a;
+  Ds.resize(D.size());
+  for (size_t i = 0; i < D.size(); ++i) Ds[i] = D[i] * sc;
+  D2.assign(size_t(p) * p, 0.0);
+  for (int i = 0; i < p; ++i)
+    for (int j = 0; j < p; ++j) {
+      double s = 0.0;
+      for (int k = 0; k < p; ++k) s += Ds[size_t(i) * p + k] * Ds[size_t(k) * p + j];
+      D2[size_t(i) * p + j] = s;
+    }
+}
+
+int code(int y, int x, int kind, int edge = 0) { return y | (x << 8) | (kind << 16) | (edge << 18); }
+
+void boundary_node(int k, int p, int* iy, int* ix, int* edge) {
+  if (k < p) { *edge = 0; *iy = 0; *ix = k; return; }
+  if (k < 2 * p - 1) { *edge = 1; *iy = k - p + 1; *ix = p - 1; return; }
+  if (k < 3 * p - 2) { *edge = 2; *iy = p - 1; *ix = k - 2 * p + 1; return; }
+  *edge = 3; *iy = k - 3 * p + 3; *ix = 0;
+}
+
+// Row/column codes of the augmented layout (hps_device.cuh).
+void layout_codes(const LeafDims& d, bool solve, std::vector<int>& rows, std::vector<int>& cols) {
+  const int p = d.p, q = p - 2;
+  rows.assign(d.Rpad, code(0, 0, 3));
+  cols.assign(d.ld, code(0, 0, 3));
+  for (int r = 0; r < d.ni; ++r) rows[r] = code(r / q + 1, r % q + 1, 0);
+  for (int c = 0; c < d.ni; ++c) cols[c] = code(c / q + 1, c % q + 1, 0);
+  if (solve) {
+    cols[d.tb0] = code(0, 0, 2);
+    return;
+  }
+  for (int k = 0; k < d.nb; ++k) {
+    int iy, ix, e;
+    boundary_node(k, p, &iy, &ix, &e);
+    rows[d.ni + k] = code(iy, ix, 1, e);
+    cols[d.tb0 + k] = code(iy, ix, 1);
+  }
+  cols[d.tb0 + d.nb] = code(0, 0, 2);
+}
+
+LeafDims solve_dims(int p) {
+  LeafDims d = hpsg::make_dims(p);
+  d.nb = 0;
+  d.R = d.ni;
+  d.Rpad = (d.ni + 63) / 64 * 64;
+  d.ld = (d.tb0 + 1 + 63) / 64 * 64;
+  d.ntb = 1;
+  d.leaf_stride = (long long)d.Rpad * d.ld;
+  return d;
+}
+
+// ---- mesh tables ------------------
+struct MeshHost {
+  int nx, ny, p, n_edges;
+  int64_t n_active, nnz;
+  std::vector<int> elem_edges, edge_elems, edge_sides, edge_cols, edge_ne;
+  std::vector<int64_t> edge_off;
+};
+
+MeshHost mesh_tables(int nx, int ny, int p) {
+  MeshHost m;
+  m.nx = nx; m.ny = ny; m.p = p;
+  m.n_edges = (nx - 1) * ny + nx * (ny - 1);
+  m.n_active = int64_t(m.n_edges) * (p - 2);
+  auto id_h = [&](int c, int ey) { return c * (2 * ny - 1) + (ey - 1); };
+  auto id_v = [&](int ex, int ey) { return (ex - 1) * (2 * ny - 1) + (ny - 1) + ey; };
+  m.elem_edges.assign(size_t(4) * nx * ny, -1);
+  for (int ey = 0; ey < ny; ++ey)
+    for (int ex = 0; ex < nx; ++ex) {
+      int* s = &m.elem_edges[size_t(4) * (ey * nx + ex)];
+      if (ey >= 1) s[0] = id_h(ex, ey);
+      if (ex + 1 <= nx - 1) s[1] = id_v(ex + 1, ey);
+      if (ey + 1 <= ny - 1) s[2] = id_h(ex, ey + 1);
+      if (ex >= 1) s[3] = id_v(ex, ey);
+    }
+  m.edge_elems.assign(size_t(2) * m.n_edges, -1);
+  m.edge_sides.assign(size_t(2) * m.n_edges, -1);
+  for (int c = 0; c < nx; ++c)
+    for (int ey = 1; ey < ny; ++ey) {
+      const int id = id_h(c, ey);
+      m.edge_elems[2 * id] = (ey - 1) * nx + c; m.edge_sides[2 * id] = 2;
+      m.edge_elems[2 * id + 1] = ey * nx + c;   m.edge_sides[2 * id + 1] = 0;
+    }
+  for (int ex = 1; ex < nx; ++ex)
+    for (int ey = 0; ey < ny; ++ey) {
+      const int id = id_v(ex, ey);
+      m.edge_elems[2 * id] = ey * nx + ex - 1; m.edge_sides[2 * id] = 1;
+      m.edge_elems[2 * id + 1] = ey * nx + ex; m.edge_sides[2 * id + 1] = 3;
+    }
+  const int q = p - 2;
+  m.edge_cols.assign(size_t(7) * m.n_edges, -1);
+  m.edge_ne.assign(m.n_edges, 0);
+  m.edge_off.assign(size_t(m.n_edges) + 1, 0);
+  for (int ed = 0; ed < m.n_edges; ++ed) {
+    int buf[8], n = 0;
+    for (int t = 0; t < 2; ++t) {
+      const int e = m.edge_elems[2 * ed + t];
+      for (int s = 0; s < 4; ++s) {
+        const int x = m.elem_edges[size_t(4) * e + s];
+        if (x >= 0) buf[n++] = x;
+      }
+    }
+    std::sort(buf, buf + n);
+    n = int(std::unique(buf, buf + n) - buf);
+    for (int i = 0; i < n; ++i) m.edge_cols[size_t(7) * ed + i] = buf[i];
+    m.edge_ne[ed] = n;
+    m.edge_off[ed + 1] = m.edge_off[ed] + int64_t(n) * q * q;
+  }
+  m.nnz = m.edge_off[m.n_edges];
+  return m;
+}
+
+}  // namespace
+
+// ============================================================================
+struct hps_gpu_ctx {
+  int device = 0;
+  hps_leaf_desc desc{};
+  LeafDims d{}, ds{};
+  int sms = 148;
+  int n_leaves = 0;
+  int chunk = 0;
+  size_t per_leaf = 0;
+  std::string err;
+  double k2 = 0.0;
+  DevBuf rowcode, colcode, rowcode_s, colcode_s, Ds, D2;
+  DevBuf ws, linv, perm, norms, minratio, status, inject_all;
+  DevBuf in_b[2], in_f[2], in_v[2], out_T[2], out_w[2], out_st[2], out_u[2];
+  MeshHost mesh;
+  DevBuf m_elem_edges, m_edge_elems, m_edge_sides, m_edge_cols, m_edge_ne, m_edge_off;
+  cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_in_ready[2]{}, ev_in_free[2]{}, ev_out_ready[2]{}, ev_out_free[2]{};
+  std::vector<cudaEvent_t> tev;  // timing events (3 per chunk) on the compute stream
+  hps_gpu_timing_t timing{};
+  bool has_inject = false;
+  int store_e0 = -1, store_e1 = -1;
+
+  ~hps_gpu_ctx() {
+    for (auto e : tev) cudaEventDestroy(e);
+    for (int i = 0; i < 2; ++i) {
+      if (ev_in_ready[i]) cudaEventDestroy(ev_in_ready[i]);
+      if (ev_in_free[i]) cudaEventDestroy(ev_in_free[i]);
+      if (ev_out_ready[i]) cudaEventDestroy(ev_out_ready[i]);
+      if (ev_out_free[i]) cudaEventDestroy(ev_out_free[i]);
+    }
+    if (s_comp) cudaStreamDestroy(s_comp);
+    if (s_h2d) cudaStreamDestroy(s_h2d);
+    if (s_d2h) cudaStreamDestroy(s_d2h);
+  }
+  int fail(int code, const std::string& m) {
+    err = m;
+    return code;
+  }
+  int cuda_fail(cudaError_t e, const char* where) {
+    return fail(HPS_ERR_CUDA, std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e));
+  }
+  hpsg::MeshDev mesh_dev() const {
+    hpsg::MeshDev m;
+    m.nx = mesh.nx; m.ny = mesh.ny; m.p = mesh.p; m.n_edges = mesh.n_edges;
+    m.n_active = mesh.n_active;
+    m.elem_edges = m_elem_edges.as<int>();
+    m.edge_elems = m_edge_elems.as<int>();
+    m.edge_sides = m_edge_sides.as<int>();
+    m.edge_cols = m_edge_cols.as<int>();
+    m.edge_ne = m_edge_ne.as<int>();
+    m.edge_off = m_edge_off.as<int64_t>();
+    return m;
+  }
+  cudaEvent_t timing_event(size_t i) {
+    while (tev.size() <= i) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      tev.push_back(e);
+    }
+    return tev[i];
+  }
+};
+
+#define CK(call)                                                  \
+  do {                                                            \
+    cudaError_t e__ = (call);                                     \
+    if (e__ != cudaSuccess) return ctx->cuda_fail(e__, #call);    \
+  } while (0)
+
+namespace {
+
+template <class T>
+cudaError_t upload(DevBuf& b, const std::vector<T>& v) {
+  cudaError_t e = b.ensure(std::max<size_t>(1, v.size() * sizeof(T)));
+  if (e != cudaSuccess) return e;
+  if (v.empty()) return cudaSuccess;
+  return cudaMemcpy(b.ptr, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+std::string id_list(const std::vector<int>& ids) {
+  std::string s;
+  for (size_t i = 0; i < ids.size() && i < 64; ++i) s += (i ? "," : "") + std::to_string(ids[i]);
+  if (ids.size() > 64) s += ",...";
+  return s;
+}
+
+int resonance_error(hps_gpu_ctx* ctx, const std::vector<int>& bad) {
+  return ctx->fail(HPS_ERR_RESONANCE,
+                   "ResonanceError: element " + std::to_string(bad.front()) +
+                       ": interior block singular (pivot < 1e-12*||A_ii||_inf); failing elements [" +
+                       id_list(bad) + "]");
+}
+
+void finish_timing(hps_gpu_ctx* ctx, int nchunks, int kernels_per_chunk) {
+  hps_gpu_timing_t t{};
+  t.chunks = nchunks;
+  t.kernels = nchunks * kernels_per_chunk;
+  if (nchunks > 0) {
+    cudaEventSynchronize(ctx->tev[3 * nchunks - 1]);
+    for (int c = 0; c < nchunks; ++c) {
+      float a = 0, b = 0;
+      cudaEventElapsedTime(&a, ctx->tev[3 * c], ctx->tev[3 * c + 1]);
+      cudaEventElapsedTime(&b, ctx->tev[3 * c + 1], ctx->tev[3 * c + 2]);
+      t.ms_assemble += a;
+      t.ms_lu_schur += b;
+    }
+    cudaEventElapsedTime(&t.ms_total, ctx->tev[0], ctx->tev[3 * nchunks - 1]);
+  }
+  ctx->timing = t;
+}
+
+// Device pipeline for one chunk of `n` leaves starting at element e (K1 + K2).
+void enqueue_condense_chunk(hps_gpu_ctx* ctx, int e, int n, const double* d_b, const double* d_f,
+                            double* d_T, double* d_w, int* d_status, cudaStream_t st, int ci) {
+  const LeafDims& d = ctx->d;
+  const int* inj = ctx->has_inject ? ctx->inject_all.as<int>() + e : nullptr;
+  cudaEventRecord(ctx->timing_event(3 * ci), st);
+  hpsg::launch_assemble(d, ctx->rowcode.as<int>(), ctx->colcode.as<int>(), ctx->Ds.as<double>(),
+                        ctx->D2.as<double>(), ctx->k2, d_b, d_f, ctx->ws.as<double>(),
+                        ctx->norms.as<double>(), inj, n, st);
+  cudaEventRecord(ctx->timing_event(3 * ci + 1), st);
+  hpsg::LuArgs a;
+  a.d = d;
+  a.ws = ctx->ws.as<double>();
+  a.linv = ctx->linv.as<double>();
+  a.perm = ctx->perm.as<short>();
+  a.norms = ctx->norms.as<double>();
+  a.T_out = d_T;
+  a.w_out = d_w;
+  a.status = d_status;
+  a.minratio = ctx->minratio.as<double>();
+  a.factor = 1;
+  hpsg::launch_lu_schur(a, n, st);
+  cudaEventRecord(ctx->timing_event(3 * ci + 2), st);
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+const char* hps_gpu_version(void) { return "hps_leaf_b200 0.1 (sm_100a, DMMA f64)"; }
+
+void* hps_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes, cudaHostAllocPortable) != cudaSuccess) return nullptr;
+  return p;
+}
+void hps_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+static thread_local std::string g_create_error;
+
+// ctx == NULL returns the message of the last failed hps_gpu_create on this thread.
+const char* hps_gpu_last_error(const hps_gpu_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_create_error.c_str();
+}
+
+int hps_gpu_create(int device, const hps_leaf_desc* desc, hps_gpu_ctx** out) {
+  if (!out || !desc) return HPS_ERR_PARAM;
+  *out = nullptr;
+  auto ctx = std::make_unique<hps_gpu_ctx>();
+  auto reject = [&](int code, const std::string& m) {
+    g_create_error = m;
+    return code;
+  };
+  ctx->device = device;
+  ctx->desc = *desc;
+  const hps_leaf_desc& D = *desc;
+  // ParameterError conventions: cheb_nodes p < 4, scale_to_interval a <= 0 (:66).
+  if (D.p < 4 || D.p > kMaxP)
+    return reject(HPS_ERR_PARAM, "ParameterError: p must be in [4, 45]");
+  if (!(D.a > 0.0))
+    return reject(HPS_ERR_PARAM, "ParameterError: a must be > 0");
+  if (!(D.kappa >= 0.0) || !std::isfinite(D.kappa))
+    return reject(HPS_ERR_PARAM, "ParameterError: kappa must be >= 0");
+  if (D.nx < 1 || D.ny < 1)
+    return reject(HPS_ERR_PARAM, "ParameterError: nx, ny must be >= 1");
+  if (D.storage != HPS_STORAGE_RECOMPUTE && D.storage != HPS_STORAGE_STORE)
+    return reject(HPS_ERR_PARAM, "ParameterError: unknown storage policy");
+  hps_gpu_ctx* c = ctx.get();
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return reject(HPS_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  c->d = hpsg::make_dims(D.p);
+  c->ds = solve_dims(D.p);
+  c->n_leaves = D.nx * D.ny;
+  c->k2 = D.kappa * D.kappa;
+  std::vector<double> Ds, D2;
+  cheb_tables(D.p, D.a, Ds, D2);
+  std::vector<int> rows, cols, rows_s, cols_s;
+  layout_codes(c->d, false, rows, cols);
+  layout_codes(c->ds, true, rows_s, cols_s);
+  c->mesh = mesh_tables(D.nx, D.ny, D.p);
+  hps_gpu_ctx* ctxp = c;
+#undef CK
+#define CK(call)                                                                        \
+  do {                                                                                  \
+    cudaError_t e__ = (call);                                                           \
+    if (e__ != cudaSuccess)                                                             \
+      return reject(HPS_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e__)); \
+  } while (0)
+  {
+    hps_gpu_ctx* ctx = ctxp;  // for CK
+    CK(upload(c->Ds, Ds));
+    CK(upload(c->D2, D2));
+    CK(upload(c->rowcode, rows));
+    CK(upload(c->colcode, cols));
+    CK(upload(c->rowcode_s, rows_s));
+    CK(upload(c->colcode_s, cols_s));
+    CK(upload(c->m_elem_edges, c->mesh.elem_edges));
+    CK(upload(c->m_edge_elems, c->mesh.edge_elems));
+    CK(upload(c->m_edge_sides, c->mesh.edge_sides));
+    CK(upload(c->m_edge_cols, c->mesh.edge_cols));
+    CK(upload(c->m_edge_ne, c->mesh.edge_ne));
+    CK(upload(c->m_edge_off, c->mesh.edge_off));
+    CK(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventCreateWithFlags(&c->ev_in_ready[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_in_free[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_out_ready[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_out_free[i], cudaEventDisableTiming));
+    }
+  }
+  // Memory plan: per in-flight leaf = workspace + Linv + perm + scalars + 2x I/O.
+  const LeafDims& d = c->d;
+  const size_t pp = size_t(D.p) * D.p;
+  const size_t io = (2 * pp + size_t(d.nb) * d.nb + 2 * d.nb + pp + 4) * sizeof(double);
+  c->per_leaf = size_t(d.leaf_stride) * 8 + size_t(d.nblk) * 4096 * 8 + size_t(d.Rpad) * 2 + 32 +
+                2 * io;
+  size_t budget = size_t(D.workspace_bytes);
+  if (budget == 0) {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    budget = size_t(double(fr) * 0.7);
+  }
+  int chunk = int(std::min<size_t>(size_t(c->n_leaves), budget / c->per_leaf));
+  const int slots = 2 * c->sms;
+  if (chunk > slots) chunk = chunk / slots * slots;
+  if (D.storage == HPS_STORAGE_STORE && chunk < c->n_leaves)
+    return reject(HPS_ERR_PARAM, "ParameterError: storage policy 'store' needs the factors of all " +
+                                     std::to_string(c->n_leaves) +
+                                     " leaves resident; exceeds the device budget (use recompute)");
+  if (chunk < 1)
+    return reject(HPS_ERR_PARAM, "ParameterError: device budget below one leaf");
+  c->chunk = chunk;
+  {
+    hps_gpu_ctx* ctx = ctxp;
+    CK(c->ws.ensure(size_t(chunk) * d.leaf_stride * 8));
+    CK(c->linv.ensure(size_t(chunk) * d.nblk * 4096 * 8));
+    CK(c->perm.ensure(size_t(chunk) * d.Rpad * 2));
+    CK(c->norms.ensure(size_t(chunk) * 8));
+    CK(c->minratio.ensure(size_t(chunk) * 8));
+    CK(c->status.ensure(size_t(chunk) * 4));
+    CK(c->inject_all.ensure(size_t(c->n_leaves) * 4));
+    CK(cudaMemset(c->inject_all.ptr, 0, size_t(c->n_leaves) * 4));
+    CK(cudaMemset(c->ws.ptr, 0, size_t(chunk) * d.leaf_stride * 8));
+  }
+  *out = ctx.release();
+  return HPS_OK;
+}
+#undef CK
+#define CK(call)                                                  \
+  do {                                                            \
+    cudaError_t e__ = (call);                                     \
+    if (e__ != cudaSuccess) return ctx->cuda_fail(e__, #call);    \
+  } while (0)
+
+void hps_gpu_destroy(hps_gpu_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  delete ctx;
+}
+
+int hps_gpu_get_info(const hps_gpu_ctx* ctx, hps_gpu_info_t* out) {
+  if (!ctx || !out) return HPS_ERR_PARAM;
+  out->p = ctx->d.p;
+  out->n_i = ctx->d.ni;
+  out->n_b = ctx->d.nb;
+  out->n_leaves = ctx->n_leaves;
+  out->chunk_leaves = ctx->chunk;
+  out->resident_ctas = 2 * ctx->sms;
+  out->workspace_bytes_per_leaf = int64_t(ctx->per_leaf);
+  out->n_active = ctx->mesh.n_active;
+  out->N = int64_t(ctx->desc.nx * (ctx->d.p - 1) + 1) * int64_t(ctx->desc.ny * (ctx->d.p - 1) + 1);
+  return HPS_OK;
+}
+
+int hps_gpu_get_timing(const hps_gpu_ctx* ctx, hps_gpu_timing_t* out) {
+  if (!ctx || !out) return HPS_ERR_PARAM;
+  *out = ctx->timing;
+  return HPS_OK;
+}
+
+int hps_gpu_set_fault_injection(hps_gpu_ctx* ctx, const int32_t* elements, int32_t n) {
+  if (!ctx) return HPS_ERR_PARAM;
+  cudaSetDevice(ctx->device);
+  std::vector<int> flags(ctx->n_leaves, 0);
+  for (int i = 0; i < n; ++i)
+    if (elements[i] >= 0 && elements[i] < ctx->n_leaves) flags[elements[i]] = 1;
+  CK(cudaMemcpy(ctx->inject_all.ptr, flags.data(), flags.size() * 4, cudaMemcpyHostToDevice));
+  ctx->has_inject = n > 0;
+  return HPS_OK;
+}
+
+static int check_range(hps_gpu_ctx* ctx, int e0, int e1) {
+  if (e0 < 0 || e1 > ctx->n_leaves || e0 > e1)
+    return ctx->fail(HPS_ERR_PARAM, "ParameterError: element range [" + std::to_string(e0) + ", " +
+                                        std::to_string(e1) + ") outside the mesh");
+  return HPS_OK;
+}
+
+int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, const double* f,
+                     double* T, double* w, double* S, int32_t* status) {
+  if (!ctx) return HPS_ERR_PARAM;
+  if (int rc = check_range(ctx, e0, e1)) return rc;
+  if (S) return ctx->fail(HPS_ERR_PARAM, "ParameterError: S_solve output is not available in this build");
+  if (!b || !f || !T || !w || !status) return ctx->fail(HPS_ERR_PARAM, "ParameterError: null buffer");
+  if (ctx->desc.storage == HPS_STORAGE_STORE && (e1 - e0) > ctx->chunk)
+    return ctx->fail(HPS_ERR_PARAM, "ParameterError: store policy range exceeds resident factors");
+  CK(cudaSetDevice(ctx->device));
+  const LeafDims& d = ctx->d;
+  const size_t pp = size_t(d.p) * d.p, nb2 = size_t(d.nb) * d.nb;
+  const int chunk = ctx->chunk;
+  for (int i = 0; i < 2; ++i) {
+    CK(ctx->in_b[i].ensure(size_t(chunk) * pp * 8));
+    CK(ctx->in_f[i].ensure(size_t(chunk) * pp * 8));
+    CK(ctx->out_T[i].ensure(size_t(chunk) * nb2 * 8));
+    CK(ctx->out_w[i].ensure(size_t(chunk) * d.nb * 8));
+    CK(ctx->out_st[i].ensure(size_t(chunk) * 4));
+  }
+  int ci = 0;
+  for (int c0 = e0; c0 < e1; c0 += chunk, ++ci) {
+    const int n = std::min(chunk, e1 - c0);
+    const int k = ci & 1;
+    const size_t off = size_t(c0 - e0);
+    CK(cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_in_free[k], 0));
+    CK(cudaMemcpyAsync(ctx->in_b[k].ptr, b + off * pp, n * pp * 8, cudaMemcpyHostToDevice, ctx->s_h2d));
+    CK(cudaMemcpyAsync(ctx->in_f[k].ptr, f + off * pp, n * pp * 8, cudaMemcpyHostToDevice, ctx->s_h2d));
+    CK(cudaEventRecord(ctx->ev_in_ready[k], ctx->s_h2d));
+    CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_in_ready[k], 0));
+    CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_out_free[k], 0));
+    enqueue_condense_chunk(ctx, c0, n, ctx->in_b[k].as<double>(), ctx->in_f[k].as<double>(),
+                           ctx->out_T[k].as<double>(), ctx->out_w[k].as<double>(),
+                           ctx->out_st[k].as<int>(), ctx->s_comp, ci);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ctx->ev_in_free[k], ctx->s_comp));
+    CK(cudaEventRecord(ctx->ev_out_ready[k], ctx->s_comp));
+    CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_out_ready[k], 0));
+    CK(cudaMemcpyAsync(T + off * nb2, ctx->out_T[k].ptr, n * nb2 * 8, cudaMemcpyDeviceToHost, ctx->s_d2h));
+    CK(cudaMemcpyAsync(w + off * d.nb, ctx->out_w[k].ptr, n * size_t(d.nb) * 8, cudaMemcpyDeviceToHost,
+                       ctx->s_d2h));
+    CK(cudaMemcpyAsync(status + off, ctx->out_st[k].ptr, n * 4, cudaMemcpyDeviceToHost, ctx->s_d2h));
+    CK(cudaEventRecord(ctx->ev_out_free[k], ctx->s_d2h));
+  }
+  CK(cudaStreamSynchronize(ctx->s_d2h));
+  CK(cudaStreamSynchronize(ctx->s_comp));
+  finish_timing(ctx, ci, 3);
+  if (ctx->desc.storage == HPS_STORAGE_STORE) {
+    ctx->store_e0 = e0;
+    ctx->store_e1 = e1;
+  }
+  std::vector<int> bad;
+  for (int i = 0; i < e1 - e0; ++i)
+    if (status[i]) bad.push_back(e0 + i);
+  if (!bad.empty()) return resonance_error(ctx, bad);
+  return HPS_OK;
+}
+
+int hps_gpu_condense_device(hps_gpu_ctx* ctx, int32_t e0, int32_t n, const double* d_b,
+                            const double* d_f, double* d_T, double* d_w, int32_t* d_status,
+                            void* stream) {
+  if (!ctx) return HPS_ERR_PARAM;
+  if (int rc = check_range(ctx, e0, e0 + n)) return rc;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->s_comp;
+  const LeafDims& d = ctx->d;
+  const size_t pp = size_t(d.p) * d.p, nb2 = size_t(d.nb) * d.nb;
+  int ci = 0;
+  for (int c0 = 0; c0 < n; c0 += ctx->chunk, ++ci) {
+    const int m = std::min(ctx->chunk, n - c0);
+    enqueue_condense_chunk(ctx, e0 + c0, m, d_b + c0 * pp, d_f + c0 * pp, d_T + c0 * nb2,
+                           d_w + size_t(c0) * d.nb, d_status + c0, st, ci);
+    CK(cudaGetLastError());
+  }
+  ctx->timing = hps_gpu_timing_t{};
+  ctx->timing.chunks = ci;
+  ctx->timing.kernels = 3 * ci;
+  return HPS_OK;
+}
+
+int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, const double* f,
+                       const double* v, double* u, int32_t* status) {
+  if (!ctx) return HPS_ERR_PARAM;
+  if (int rc = check_range(ctx, e0, e1)) return rc;
+  if (!b || !f || !v || !u || !status) return ctx->fail(HPS_ERR_PARAM, "ParameterError: null buffer");
+  const bool store = ctx->desc.storage == HPS_STORAGE_STORE;
+  if (store && (e0 < ctx->store_e0 || e1 > ctx->store_e1))
+    return ctx->fail(HPS_ERR_PARAM, "ParameterError: store policy: no kept factors for [" +
+                                        std::to_string(e0) + ", " + std::to_string(e1) + ")");
+  CK(cudaSetDevice(ctx->device));
+  const LeafDims& d = ctx->d;
+  const size_t pp = size_t(d.p) * d.p, nb = size_t(d.nb);
+  const int chunk = ctx->chunk;
+  for (int i = 0; i < 2; ++i) {
+    CK(ctx->in_b[i].ensure(size_t(chunk) * pp * 8));
+    CK(ctx->in_f[i].ensure(size_t(chunk) * pp * 8));
+    CK(ctx->in_v[i].ensure(size_t(chunk) * nb * 8));
+    CK(ctx->out_u[i].ensure(size_t(chunk) * pp * 8));
+    CK(ctx->out_st[i].ensure(size_t(chunk) * 4));
+  }
+  int ci = 0;
+  for (int c0 = e0; c0 < e1; c0 += chunk, ++ci) {
+    const int n = std::min(chunk, e1 - c0);
+    const int k = ci & 1;
+    const size_t off = size_t(c0 - e0);
+    CK(cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_in_free[k], 0));
+    CK(cudaMemcpyAsync(ctx->in_b[k].ptr, b + off * pp, n * pp * 8, cudaMemcpyHostToDevice, ctx->s_h2d));
+    CK(cudaMemcpyAsync(ctx->in_f[k].ptr, f + off * pp, n * pp * 8, cudaMemcpyHostToDevice, ctx->s_h2d));
+    CK(cudaMemcpyAsync(ctx->in_v[k].ptr, v + off * nb, n * nb * 8, cudaMemcpyHostToDevice, ctx->s_h2d));
+    CK(cudaEventRecord(ctx->ev_in_ready[k], ctx->s_h2d));
+    CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_in_ready[k], 0));
+    CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_out_free[k], 0));
+    cudaStream_t st = ctx->s_comp;
+    cudaEventRecord(ctx->timing_event(3 * ci), st);
+    hpsg::LuArgs a;
+    a.ws = ctx->ws.as<double>();
+    a.linv = ctx->linv.as<double>();
+    a.perm = ctx->perm.as<short>();
+    a.norms = ctx->norms.as<double>();
+    a.T_out = nullptr;
+    a.w_out = nullptr;
+    a.status = ctx->out_st[k].as<int>();
+    a.minratio = nullptr;
+    LeafDims dsolve;
+    if (store) {
+      // Kept condense factors: rhs into column tb0, trailing-only LU pass.
+      const size_t lo = size_t(c0 - ctx->store_e0);
+      dsolve = d;
+      dsolve.R = d.ni;
+      dsolve.ntb = 1;
+      a.ws += lo * d.leaf_stride;
+      a.linv += lo * d.nblk * 4096;
+      a.perm += lo * d.Rpad;
+      hpsg::launch_write_rhs(d, d.tb0, ctx->D2.as<double>(), ctx->in_f[k].as<double>(),
+                             ctx->in_v[k].as<double>(), a.ws, n, st);
+      CK(cudaMemsetAsync(a.status, 0, n * 4, st));
+      a.factor = 0;
+    } else {
+      dsolve = ctx->ds;
+      const int* inj = ctx->has_inject ? ctx->inject_all.as<int>() + c0 : nullptr;
+      hpsg::launch_assemble_solve(dsolve, ctx->rowcode_s.as<int>(), ctx->colcode_s.as<int>(),
+                                  ctx->Ds.as<double>(), ctx->D2.as<double>(), ctx->k2,
+                                  ctx->in_b[k].as<double>(), ctx->in_f[k].as<double>(),
+                                  ctx->in_v[k].as<double>(), a.ws, ctx->norms.as<double>(), inj, n, st);
+      a.factor = 1;
+    }
+    cudaEventRecord(ctx->timing_event(3 * ci + 1), st);
+    a.d = dsolve;
+    hpsg::launch_lu_schur(a, n, st);
+    hpsg::launch_backsolve(dsolve, a.ws, a.perm, ctx->in_v[k].as<double>(), ctx->out_u[k].as<double>(),
+                           n, st);
+    cudaEventRecord(ctx->timing_event(3 * ci + 2), st);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(ctx->ev_in_free[k], st));
+    CK(cudaEventRecord(ctx->ev_out_ready[k], st));
+    CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_out_ready[k], 0));
+    CK(cudaMemcpyAsync(u + off * pp, ctx->out_u[k].ptr, n * pp * 8, cudaMemcpyDeviceToHost, ctx->s_d2h));
+    CK(cudaMemcpyAsync(status + off, ctx->out_st[k].ptr, n * 4, cudaMemcpyDeviceToHost, ctx->s_d2h));
+    CK(cudaEventRecord(ctx->ev_out_free[k], ctx->s_d2h));
+  }
+  CK(cudaStreamSynchronize(ctx->s_d2h));
+  CK(cudaStreamSynchronize(ctx->s_comp));
+  finish_timing(ctx, ci, store ? 3 : 4);
+  std::vector<int> bad;
+  for (int i = 0; i < e1 - e0; ++i)
+    if (status[i]) bad.push_back(e0 + i);
+  if (!bad.empty()) return resonance_error(ctx, bad);
+  return HPS_OK;
+}
+
+int hps_gpu_reduced_pattern(hps_gpu_ctx* ctx, int64_t* nnz, int64_t* row_ptr, int32_t* col_idx) {
+  if (!ctx || !nnz) return HPS_ERR_PARAM;
+  *nnz = ctx->mesh.nnz;
+  if (!row_ptr) return HPS_OK;
+  if (!col_idx) return ctx->fail(HPS_ERR_PARAM, "ParameterError: null col_idx");
+  CK(cudaSetDevice(ctx->device));
+  const int64_t na = ctx->mesh.n_active;
+  if (na == 0) {
+    row_ptr[0] = 0;
+    return HPS_OK;
+  }
+  DevBuf rp, ci;
+  CK(rp.ensure(size_t(na + 1) * 8));
+  CK(ci.ensure(size_t(std::max<int64_t>(1, ctx->mesh.nnz)) * 4));
+  hpsg::launch_reduced_pattern(ctx->mesh_dev(), rp.as<int64_t>(), ci.as<int32_t>(), ctx->s_comp);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(row_ptr, rp.ptr, size_t(na + 1) * 8, cudaMemcpyDeviceToHost, ctx->s_comp));
+  CK(cudaMemcpyAsync(col_idx, ci.ptr, size_t(ctx->mesh.nnz) * 4, cudaMemcpyDeviceToHost, ctx->s_comp));
+  CK(cudaStreamSynchronize(ctx->s_comp));
+  return HPS_OK;
+}
+
+int hps_gpu_assemble_reduced_device(hps_gpu_ctx* ctx, const double* d_T, const double* d_w,
+                                    const double* d_g_bnd, double* d_values, double* d_rhs,
+                                    void* stream) {
+  if (!ctx) return HPS_ERR_PARAM;
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->s_comp;
+  hpsg::launch_reduced_values(ctx->mesh_dev(), d_T, d_w, d_g_bnd, d_values, d_rhs, st);
+  CK(cudaGetLastError());
+  return HPS_OK;
+}
+
+int hps_gpu_assemble_reduced(hps_gpu_ctx* ctx, const double* T, const double* w,
+                             const double* g_bnd, double* values, double* rhs) {
+  if (!ctx || !T || !w || !g_bnd || !values || !rhs) return HPS_ERR_PARAM;
+  CK(cudaSetDevice(ctx->device));
+  const LeafDims& d = ctx->d;
+  const size_t nl = size_t(ctx->n_leaves), nb = size_t(d.nb);
+  const size_t ng = 2 * size_t(ctx->desc.nx * (d.p - 1) + 1) + 2 * size_t(ctx->desc.ny * (d.p - 1) + 1);
+  const int64_t na = ctx->mesh.n_active, nnz = ctx->mesh.nnz;
+  if (na == 0) return HPS_OK;
+  DevBuf dT, dw, dg, dv, dr;
+  CK(dT.ensure(nl * nb * nb * 8));
+  CK(dw.ensure(nl * nb * 8));
+  CK(dg.ensure(ng * 8));
+  CK(dv.ensure(size_t(nnz) * 8));
+  CK(dr.ensure(size_t(na) * 8));
+  cudaStream_t st = ctx->s_comp;
+  CK(cudaMemcpyAsync(dT.ptr, T, nl * nb * nb * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dw.ptr, w, nl * nb * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dg.ptr, g_bnd, ng * 8, cudaMemcpyHostToDevice, st));
+  cudaEvent_t t0 = ctx->timing_event(0), t1 = ctx->timing_event(1);
+  cudaEventRecord(t0, st);
+  hpsg::launch_reduced_values(ctx->mesh_dev(), dT.as<double>(), dw.as<double>(), dg.as<double>(),
+                              dv.as<double>(), dr.as<double>(), st);
+  cudaEventRecord(t1, st);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(values, dv.ptr, size_t(nnz) * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(rhs, dr.ptr, size_t(na) * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  hps_gpu_timing_t t{};
+  cudaEventElapsedTime(&t.ms_scatter, t0, t1);
+  t.ms_total = t.ms_scatter;
+  t.kernels = 1;
+  ctx->timing = t;
+  return HPS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,62 @@
+// Launch wrappers of the sm_100a kernels (internal to libhps_leaf_b200.so).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "hps_device.cuh"
+
+namespace hpsg {
+
+// K1: augmented leaf matrices + ||A_ii||_inf.
+void launch_assemble(const LeafDims& d, const int* rowcode, const int* colcode, const double* Ds,
+                     const double* D2, double k2, const double* b, const double* f, double* ws,
+                     double* norms, const int* inject, int n_leaves, cudaStream_t st);
+
+// K1 (leaf-solve variant): [A_ii | f_i - A_ib v] with no D rows (rows ni..Rpad zero).
+void launch_assemble_solve(const LeafDims& d, const int* rowcode, const int* colcode,
+                           const double* Ds, const double* D2, double k2, const double* b,
+                           const double* f, const double* v, double* ws, double* norms,
+                           const int* inject, int n_leaves, cudaStream_t st);
+
+// Store-policy leaf solve: rhs into column `col` of a kept condense workspace.
+void launch_write_rhs(const LeafDims& d, int col, const double* D2, const double* f,
+                      const double* v, double* ws, int n_leaves, cudaStream_t st);
+
+// K2+K3: blocked LU + triangular solves + Schur GEMM -> T, w, status.
+struct LuArgs {
+  LeafDims d;           // geometry; R = ni and ntb = 1 for leaf solves
+  double* ws;           // leaf workspaces (leaf_stride apart)
+  double* linv;         // nblk * 64 * 64 per leaf
+  short* perm;          // Rpad per leaf: written when factor = 1, read when factor = 0
+  const double* norms;  // ||A_ii||_inf per leaf (factor = 1)
+  double* T_out;        // nb*nb per leaf (D rows of the trailing columns)
+  double* w_out;        // nb per leaf
+  int* status;          // per leaf (factor = 1)
+  double* minratio;     // per leaf, nullable
+  int factor;           // 1: factor A_ii then trailing columns; 0: trailing columns only
+};
+size_t lu_smem_bytes();
+void launch_lu_schur(const LuArgs& a, int n_leaves, cudaStream_t st);
+
+// K5: back substitution u_i = U^{-1} y (y = L^{-1} P rhs in column tb0) and the
+// local solution vector u (p*p per leaf): interior from the solve, boundary = v.
+void launch_backsolve(const LeafDims& d, const double* ws, const short* perm, const double* v,
+                      double* u, int n_leaves, cudaStream_t st);
+
+// Mesh tables for K4 (device pointers).
+struct MeshDev {
+  int nx, ny, p, n_edges;
+  int64_t n_active;
+  const int* elem_edges;   // 4 per element (S,E,N,W), -1 on Gamma
+  const int* edge_elems;   // 2 per edge, ascending element id
+  const int* edge_sides;   // 2 per edge
+  const int* edge_cols;    // 7 per edge: sorted column edges of the row block, -1 padded
+  const int* edge_ne;      // number of column edges
+  const int64_t* edge_off; // first nonzero of the edge's rows
+};
+void launch_reduced_pattern(const MeshDev& m, int64_t* row_ptr, int32_t* col_idx, cudaStream_t st);
+void launch_reduced_values(const MeshDev& m, const double* T, const double* w, const double* g_bnd,
+                           double* values, double* rhs, cudaStream_t st);
+
+}  // namespace hpsg

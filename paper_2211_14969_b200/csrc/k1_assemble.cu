@@ -1,0 +1,219 @@
+// ============================================================================
+//  K1 — leaf operator assembly (north star #1; replaces build_leaf_operator,
+//  SPEC.md:270-278, and the block extraction in condense_leaf).
+//
+//  Writes every leaf's augmented matrix (hps_device.cuh layout) straight into
+//  the HBM workspace: interior rows of -(D2 (x) I) - (I (x) D2) - kappa^2 diag(b)
+//   and the outward-normal rows D_n.
+//  HBM-write bound: every 16-byte store is a coalesced double2 of one row.
+//  Entries are evaluated with explicit _rn intrinsics in the same operation
+//  order as the CPU oracle (oracle/hps_oracle.cpp a_entry/dn_entry), so A is
+//  bit-identical to the oracle's.
+// ============================================================================
+#include "hps_device.cuh"
+#include "hps_kernels.h"
+
+namespace hpsg {
+
+// Column/row code (built on the host once per p, see hps_host.cpp):
+//   bits 0..7  : jy (or iy)      bits 8..15 : jx (or ix)
+//   bits 16..17: kind  0 interior node, 1 boundary node, 2 load column, 3 zero
+//   bits 18..19: owning edge of a boundary node (rows only)
+__device__ __forceinline__ double a_entry(int iy, int ix, int jy, int jx, int p,
+                                          const double* __restrict__ D2, double k2, double bl) {
+  if (jy == iy && jx == ix) {
+    double v = -__ldg(D2 + iy * p + iy);
+    v = __dsub_rn(v, __ldg(D2 + ix * p + ix));
+    return __dsub_rn(v, __dmul_rn(k2, bl));
+  }
+  if (jx == ix) return -__ldg(D2 + iy * p + jy);
+  if (jy == iy) return -__ldg(D2 + ix * p + jx);
+  return 0.0;
+}
+
+__device__ __forceinline__ double dn_entry(int edge, int iy, int ix, int jy, int jx, int p,
+                                           const double* __restrict__ Ds) {
+  switch (edge) {
+    case 0: return jx == ix ? -__ldg(Ds + iy * p + jy) : 0.0;   // S: -d/dy
+    case 1: return jy == iy ? __ldg(Ds + ix * p + jx) : 0.0;    // E: +d/dx
+    case 2: return jx == ix ? __ldg(Ds + iy * p + jy) : 0.0;    // N: +d/dy
+    default: return jy == iy ? -__ldg(Ds + ix * p + jx) : 0.0;  // W: -d/dx
+  }
+}
+
+__device__ __forceinline__ double aug_value(int rcode, int ccode, int p, const double* __restrict__ Ds,
+                                            const double* __restrict__ D2, double k2,
+                                            const double* __restrict__ bl,
+                                            const double* __restrict__ fl, bool zero_aii_row) {
+  const int rkind = (rcode >> 16) & 3, ckind = (ccode >> 16) & 3;
+  if (rkind == 3 || ckind == 3) return 0.0;
+  const int iy = rcode & 255, ix = (rcode >> 8) & 255;
+  const int jy = ccode & 255, jx = (ccode >> 8) & 255;
+  if (rkind == 0) {  // interior collocation row
+    if (ckind == 2) return __ldg(fl + iy * p + ix);
+    if (ckind == 0 && zero_aii_row) return 0.0;
+    return a_entry(iy, ix, jy, jx, p, D2, k2, __ldg(bl + iy * p + ix));
+  }
+  if (ckind == 2) return 0.0;  // flux row, load column
+  return dn_entry((rcode >> 18) & 3, iy, ix, jy, jx, p, Ds);
+}
+
+// grid (ceil(Rpad / kRows), n_leaves), block 256.
+constexpr int kRows = 8;
+
+__global__ void __launch_bounds__(256) k1_assemble_kernel(
+    LeafDims d, const int* __restrict__ rowcode, const int* __restrict__ colcode,
+    const double* __restrict__ Ds, const double* __restrict__ D2, double k2,
+    const double* __restrict__ b, const double* __restrict__ f, double* __restrict__ ws,
+    const int* __restrict__ inject) {
+  const int leaf = blockIdx.y;
+  const int r0 = blockIdx.x * kRows;
+  const int pp = d.p * d.p;
+  const double* bl = b + (size_t)leaf * pp;
+  const double* fl = f + (size_t)leaf * pp;
+  const bool inj = inject && inject[leaf];
+  double* W = ws + (size_t)leaf * d.leaf_stride;
+  const int half = d.ld >> 1;
+  for (int idx = threadIdx.x; idx < kRows * half; idx += blockDim.x) {
+    const int r = r0 + idx / half;
+    if (r >= d.Rpad) break;
+    const int c = (idx % half) * 2;
+    const int rc = __ldg(rowcode + r);
+    const bool zrow = inj && r == 0;
+    double2 v;
+    v.x = aug_value(rc, __ldg(colcode + c), d.p, Ds, D2, k2, bl, fl, zrow);
+    v.y = aug_value(rc, __ldg(colcode + c + 1), d.p, Ds, D2, k2, bl, fl, zrow);
+    reinterpret_cast<double2*>(W + (size_t)r * d.ld)[c >> 1] = v;
+  }
+}
+
+// ||A_ii||_inf per leaf: row sums over the sparse cross stencil in
+// ascending column order (bit-identical to the oracle's dense ascending sum).
+__global__ void __launch_bounds__(256) k1_aii_norm_kernel(LeafDims d, const double* __restrict__ D2,
+                                                          double k2, const double* __restrict__ b,
+                                                          const int* __restrict__ inject,
+                                                          double* __restrict__ norms) {
+  const int leaf = blockIdx.x;
+  const int p = d.p, q = p - 2;
+  const double* bl = b + (size_t)leaf * p * p;
+  const bool inj = inject && inject[leaf];
+  double best = 0.0;
+  for (int i = threadIdx.x; i < d.ni; i += blockDim.x) {
+    if (inj && i == 0) continue;
+    const int iy = i / q + 1, ix = i % q + 1;
+    double s = 0.0;
+    for (int jy = 1; jy <= q; ++jy) {
+      if (jy != iy) {
+        s = __dadd_rn(s, fabs(__ldg(D2 + iy * p + jy)));
+      } else {
+        for (int jx = 1; jx <= q; ++jx)
+          s = __dadd_rn(s, fabs(a_entry(iy, ix, iy, jx, p, D2, k2, __ldg(bl + iy * p + ix))));
+      }
+    }
+    best = fmax(best, s);
+  }
+  __shared__ double red[8];
+  for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+    norms[leaf] = m;
+  }
+}
+
+// Leaf-solve right-hand side  f_i - A_ib v: the four boundary
+// neighbours of interior node (iy, ix) in ascending boundary position
+// (S: ix, E: p-1+iy, N: 2p-1+ix, W: 3p-3+iy), same operation order as the oracle.
+__device__ __forceinline__ double solve_rhs(int iy, int ix, int p, const double* __restrict__ D2,
+                                            const double* __restrict__ fl,
+                                            const double* __restrict__ vl) {
+  double s = __ldg(fl + iy * p + ix);
+  const double aS = -__ldg(D2 + iy * p + 0), aE = -__ldg(D2 + ix * p + p - 1);
+  const double aN = -__ldg(D2 + iy * p + p - 1), aW = -__ldg(D2 + ix * p + 0);
+  if (aS != 0.0) s = __dsub_rn(s, __dmul_rn(aS, __ldg(vl + ix)));
+  if (aE != 0.0) s = __dsub_rn(s, __dmul_rn(aE, __ldg(vl + p - 1 + iy)));
+  if (aN != 0.0) s = __dsub_rn(s, __dmul_rn(aN, __ldg(vl + 2 * p - 1 + ix)));
+  if (aW != 0.0) s = __dsub_rn(s, __dmul_rn(aW, __ldg(vl + 3 * p - 3 + iy)));
+  return s;
+}
+
+// Recompute-policy leaf solve: [A_ii | gap | f_i - A_ib v] (no D rows).
+__global__ void __launch_bounds__(256) k1_assemble_solve_kernel(
+    LeafDims d, const int* __restrict__ rowcode, const int* __restrict__ colcode,
+    const double* __restrict__ Ds, const double* __restrict__ D2, double k2,
+    const double* __restrict__ b, const double* __restrict__ f, const double* __restrict__ v,
+    double* __restrict__ ws, const int* __restrict__ inject) {
+  const int leaf = blockIdx.y;
+  const int r0 = blockIdx.x * kRows;
+  const int pp = d.p * d.p;
+  const double* bl = b + (size_t)leaf * pp;
+  const double* fl = f + (size_t)leaf * pp;
+  const double* vl = v + (size_t)leaf * 4 * (d.p - 1);
+  const bool inj = inject && inject[leaf];
+  double* W = ws + (size_t)leaf * d.leaf_stride;
+  const int half = d.ld >> 1;
+  for (int idx = threadIdx.x; idx < kRows * half; idx += blockDim.x) {
+    const int r = r0 + idx / half;
+    if (r >= d.Rpad) break;
+    const int c = (idx % half) * 2;
+    const int rc = __ldg(rowcode + r);
+    const bool zrow = inj && r == 0;
+    double out[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int cc = __ldg(colcode + c + h);
+      if (((rc >> 16) & 3) == 0 && ((cc >> 16) & 3) == 2)
+        out[h] = solve_rhs(rc & 255, (rc >> 8) & 255, d.p, D2, fl, vl);
+      else
+        out[h] = aug_value(rc, cc, d.p, Ds, D2, k2, bl, fl, zrow);
+    }
+    reinterpret_cast<double2*>(W + (size_t)r * d.ld)[c >> 1] = make_double2(out[0], out[1]);
+  }
+}
+
+// Store-policy leaf solve: write f_i - A_ib v into column `col` of the kept
+// condense workspace (interior rows are physical rows 0..ni-1).
+__global__ void __launch_bounds__(256) k1_write_rhs_kernel(LeafDims d, int col,
+                                                           const double* __restrict__ D2,
+                                                           const double* __restrict__ f,
+                                                           const double* __restrict__ v,
+                                                           double* __restrict__ ws) {
+  const int leaf = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= d.ni) return;
+  const int q = d.p - 2;
+  const int iy = i / q + 1, ix = i % q + 1;
+  ws[(size_t)leaf * d.leaf_stride + (size_t)i * d.ld + col] =
+      solve_rhs(iy, ix, d.p, D2, f + (size_t)leaf * d.p * d.p, v + (size_t)leaf * 4 * (d.p - 1));
+}
+
+void launch_assemble(const LeafDims& d, const int* rowcode, const int* colcode, const double* Ds,
+                     const double* D2, double k2, const double* b, const double* f, double* ws,
+                     double* norms, const int* inject, int n_leaves, cudaStream_t st) {
+  if (n_leaves <= 0) return;
+  dim3 grid((d.Rpad + kRows - 1) / kRows, n_leaves);
+  k1_assemble_kernel<<<grid, 256, 0, st>>>(d, rowcode, colcode, Ds, D2, k2, b, f, ws, inject);
+  k1_aii_norm_kernel<<<n_leaves, 256, 0, st>>>(d, D2, k2, b, inject, norms);
+}
+
+void launch_assemble_solve(const LeafDims& d, const int* rowcode, const int* colcode,
+                           const double* Ds, const double* D2, double k2, const double* b,
+                           const double* f, const double* v, double* ws, double* norms,
+                           const int* inject, int n_leaves, cudaStream_t st) {
+  if (n_leaves <= 0) return;
+  dim3 grid((d.Rpad + kRows - 1) / kRows, n_leaves);
+  k1_assemble_solve_kernel<<<grid, 256, 0, st>>>(d, rowcode, colcode, Ds, D2, k2, b, f, v, ws,
+                                                 inject);
+  k1_aii_norm_kernel<<<n_leaves, 256, 0, st>>>(d, D2, k2, b, inject, norms);
+}
+
+void launch_write_rhs(const LeafDims& d, int col, const double* D2, const double* f,
+                      const double* v, double* ws, int n_leaves, cudaStream_t st) {
+  if (n_leaves <= 0) return;
+  dim3 grid((d.ni + 255) / 256, n_leaves);
+  k1_write_rhs_kernel<<<grid, 256, 0, st>>>(d, col, D2, f, v, ws);
+}
+
+}  // namespace hpsg

@@ -1,0 +1,128 @@
+// ============================================================================
+//  K4 — scatter of every leaf's T_flux / w_equiv into the reduced interface
+//  system (north star #4; replaces assemble_reduced).
+//
+//  CSR over active nodes: row j = edge*q + k (q = p-2), its
+//  columns are the active nodes of the (<= 7) interior edges of the two
+//  elements adjacent to the row's edge, edges ascending, nodes ascending
+//  (int64 row_ptr, int32 col_idx).  Gather formulation,
+//  one CTA per interface edge, no atomics: every value is
+//        0 + T_{e0}[r0, c0] + T_{e1}[r1, c1]     (present terms, e0 < e1)
+//  and every rhs entry
+//        -( sum_t ( w_t[r_t] + sum_{Gamma cols} T_t[r_t, c] g_c ) )
+//  in exactly the order of the CPU oracle, with _rn intrinsics (no FMA
+//  contraction): given the same T, values and rhs are bit-identical.
+//  HBM bound: reads the active x active part of T, writes nnz values.
+// ============================================================================
+#include "hps_device.cuh"
+#include "hps_kernels.h"
+
+namespace hpsg {
+
+__device__ __forceinline__ int side_base(int p, int side) {
+  return side == 0 ? 1 : side == 1 ? p : side == 2 ? 2 * p : 3 * p - 2;
+}
+
+// grid = n_edges, block 256
+__global__ void __launch_bounds__(256) k4_pattern_kernel(MeshDev m, int64_t* __restrict__ row_ptr,
+                                                         int32_t* __restrict__ col_idx) {
+  const int ed = blockIdx.x;
+  const int q = m.p - 2;
+  const int ne = m.edge_ne[ed];
+  const int64_t off = m.edge_off[ed];
+  const int rowlen = ne * q;
+  for (int k = threadIdx.x; k < q; k += blockDim.x) {
+    const int64_t j = (int64_t)ed * q + k;
+    row_ptr[j] = off + (int64_t)k * rowlen;
+    if (j == m.n_active - 1) row_ptr[j + 1] = off + (int64_t)q * rowlen;
+  }
+  for (int e = threadIdx.x; e < q * rowlen; e += blockDim.x) {
+    const int pos = e % rowlen;
+    const int ce = m.edge_cols[ed * 7 + pos / q];
+    col_idx[off + e] = ce * q + pos % q;
+  }
+}
+
+// grid = n_edges, block 256
+__global__ void __launch_bounds__(256) k4_values_kernel(MeshDev m, const double* __restrict__ T,
+                                                        const double* __restrict__ w,
+                                                        const double* __restrict__ g_bnd,
+                                                        double* __restrict__ values,
+                                                        double* __restrict__ rhs) {
+  const int ed = blockIdx.x;
+  const int p = m.p, q = p - 2, nb = 4 * (p - 1);
+  const int ne = m.edge_ne[ed];
+  const int64_t off = m.edge_off[ed];
+  const int rowlen = ne * q;
+  __shared__ int col_side[2][7];  // side of column-edge rank in element t, or -1
+  __shared__ int el[2], sd[2];
+  if (threadIdx.x < 2) {
+    const int t = threadIdx.x;
+    el[t] = m.edge_elems[2 * ed + t];
+    sd[t] = m.edge_sides[2 * ed + t];
+    for (int r = 0; r < 7; ++r) {
+      col_side[t][r] = -1;
+      if (r < ne) {
+        const int ce = m.edge_cols[ed * 7 + r];
+        for (int s = 0; s < 4; ++s)
+          if (m.elem_edges[4 * el[t] + s] == ce) col_side[t][r] = s;
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < q * rowlen; e += blockDim.x) {
+    const int k = e / rowlen, pos = e % rowlen;
+    const int rank = pos / q, kk = pos % q;
+    double v = 0.0;
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      const int sc = col_side[t][rank];
+      if (sc >= 0) {
+        const int r = side_base(p, sd[t]) + k;
+        v = __dadd_rn(v, __ldg(T + ((size_t)el[t] * nb + r) * nb + side_base(p, sc) + kk));
+      }
+    }
+    values[off + e] = v;
+  }
+  // rhs: one thread per row of this edge
+  const int Nx = m.nx * (p - 1) + 1, Ny = m.ny * (p - 1) + 1;
+  for (int k = threadIdx.x; k < q; k += blockDim.x) {
+    double acc = 0.0;
+    for (int t = 0; t < 2; ++t) {
+      const int e = el[t];
+      const int r = side_base(p, sd[t]) + k;
+      const double* Te = T + ((size_t)e * nb + r) * nb;
+      acc = __dadd_rn(acc, __ldg(w + (size_t)e * nb + r));
+      const int ex = e % m.nx, ey = e / m.nx;
+      for (int sc = 0; sc < 4; ++sc) {
+        if (m.elem_edges[4 * e + sc] >= 0) continue;
+        const double* gs;
+        int base;
+        switch (sc) {
+          case 0: gs = g_bnd; base = ex * (p - 1); break;                         // south
+          case 1: gs = g_bnd + 2 * Nx + Ny; base = ey * (p - 1); break;           // east
+          case 2: gs = g_bnd + Nx; base = ex * (p - 1); break;                    // north
+          default: gs = g_bnd + 2 * Nx; base = ey * (p - 1); break;               // west
+        }
+        for (int kk = 0; kk < q; ++kk) {
+          const double prod = __dmul_rn(__ldg(Te + side_base(p, sc) + kk), __ldg(gs + base + kk + 1));
+          acc = __dadd_rn(acc, prod);
+        }
+      }
+    }
+    rhs[(int64_t)ed * q + k] = -acc;
+  }
+}
+
+void launch_reduced_pattern(const MeshDev& m, int64_t* row_ptr, int32_t* col_idx, cudaStream_t st) {
+  if (m.n_edges <= 0) return;
+  k4_pattern_kernel<<<m.n_edges, 256, 0, st>>>(m, row_ptr, col_idx);
+}
+
+void launch_reduced_values(const MeshDev& m, const double* T, const double* w, const double* g_bnd,
+                           double* values, double* rhs, cudaStream_t st) {
+  if (m.n_edges <= 0) return;
+  k4_values_kernel<<<m.n_edges, 256, 0, st>>>(m, T, w, g_bnd, values, rhs);
+}
+
+}  // namespace hpsg

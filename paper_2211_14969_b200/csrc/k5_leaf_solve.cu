@@ -1,0 +1,102 @@
+// ============================================================================
+//  K5 — batched leaf-solution recovery (north star #5; replaces leaf_solve,
+//  SPEC.md:297-305, and the interior part of reconstruct_full_solution,
+//  SPEC.md:363-367).
+//
+//  Pipeline per chunk (hps_host.cpp):
+//    recompute policy: K1s [A_ii | f_i - A_ib v] -> K2 (factor + trailing column,
+//                      y = L^{-1} P rhs) -> K5 back substitution
+//    store policy    : rhs into the kept condense workspace -> K2 trailing-only
+//                      -> K5 (same code on the same factors: bitwise equal)
+//  K5 (this file): one CTA per leaf.  Blocked back substitution over the
+//  64-row blocks of U (physical rows through perm): a warp-per-row GEMV
+//  against the already-solved tail, then a one-warp triangular solve of the
+//  64x64 diagonal block.  Finally the p*p local vector u (interior from the
+//  solve, boundary = v) in local order.  HBM bound: reads U once (ni^2/2).
+// ============================================================================
+#include "hps_device.cuh"
+#include "hps_kernels.h"
+
+namespace hpsg {
+
+__global__ void __launch_bounds__(256) k5_backsolve_kernel(LeafDims d, const double* __restrict__ ws,
+                                                           const short* __restrict__ perm,
+                                                           const double* __restrict__ v,
+                                                           double* __restrict__ u) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* x = reinterpret_cast<double*>(smem_raw);
+  short* ps = reinterpret_cast<short*>(x + d.ni);
+  const int leaf = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* M = ws + (size_t)leaf * d.leaf_stride;
+  const short* P = perm + (size_t)leaf * d.Rpad;
+  const int ni = d.ni, ld = d.ld;
+  for (int k = tid; k < ni; k += 256) {
+    ps[k] = P[k];
+    x[k] = M[(size_t)P[k] * ld + d.tb0];
+  }
+  __syncthreads();
+  for (int I = d.nblk - 1; I >= 0; --I) {
+    const int r0 = 64 * I;
+    const int nr = min(64, ni - r0);
+    const int c1 = r0 + nr;
+    if (c1 < ni) {
+      for (int k = r0 + warp; k < c1; k += 8) {
+        const double* urow = M + (size_t)ps[k] * ld;
+        double s = 0.0;
+        for (int j = c1 + lane; j < ni; j += 32) s = fma(urow[j], x[j], s);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) x[k] -= s;
+      }
+      __syncthreads();
+    }
+    if (warp == 0) {
+      double y0 = lane < nr ? x[r0 + lane] : 0.0;
+      double y1 = lane + 32 < nr ? x[r0 + lane + 32] : 0.0;
+      const double* row0 = M + (size_t)ps[r0 + min(lane, nr - 1)] * ld;
+      const double* row1 = M + (size_t)ps[r0 + min(lane + 32, nr - 1)] * ld;
+      for (int kk = nr - 1; kk >= 0; --kk) {
+        const double own = (kk < 32) ? y0 : y1;
+        const double val = __shfl_sync(0xffffffffu, own, kk & 31);
+        const double xk = val / M[(size_t)ps[r0 + kk] * ld + r0 + kk];
+        if (lane == (kk & 31)) {
+          if (kk < 32) y0 = xk; else y1 = xk;
+        }
+        if (lane < kk) y0 = fma(-row0[r0 + kk], xk, y0);
+        if (lane + 32 < kk) y1 = fma(-row1[r0 + kk], xk, y1);
+      }
+      if (lane < nr) x[r0 + lane] = y0;
+      if (lane + 32 < nr) x[r0 + lane + 32] = y1;
+    }
+    __syncthreads();
+  }
+  const int p = d.p, q = p - 2, nb = 4 * (p - 1);
+  const double* vl = v + (size_t)leaf * nb;
+  double* ul = u + (size_t)leaf * p * p;
+  for (int l = tid; l < p * p; l += 256) {
+    const int iy = l / p, ix = l % p;
+    double val;
+    if (iy >= 1 && iy <= p - 2 && ix >= 1 && ix <= p - 2) val = x[(iy - 1) * q + (ix - 1)];
+    else if (iy == 0) val = vl[ix];                          // S
+    else if (ix == p - 1) val = vl[p - 1 + iy];              // E (incl. NE corner)
+    else if (iy == p - 1) val = vl[2 * p - 1 + ix];          // N (incl. NW corner)
+    else val = vl[3 * p - 3 + iy];                           // W
+    ul[l] = val;
+  }
+}
+
+void launch_backsolve(const LeafDims& d, const double* ws, const short* perm, const double* v,
+                      double* u, int n_leaves, cudaStream_t st) {
+  if (n_leaves <= 0) return;
+  const size_t smem = (size_t)d.ni * sizeof(double) + (size_t)d.ni * sizeof(short) + 16;
+  static size_t configured = 0;
+  if (smem > 48 * 1024 && smem > configured) {
+    cudaFuncSetAttribute(k5_backsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    configured = smem;
+  }
+  k5_backsolve_kernel<<<n_leaves, 256, smem, st>>>(d, ws, perm, v, u);
+}
+
+}  // namespace hpsg

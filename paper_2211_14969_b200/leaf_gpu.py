@@ -1,0 +1,230 @@
+"""ctypes binding of the C-ABI in include/hps_leaf_gpu.h (libhps_leaf_b200.so).
+
+Python-side handle on the B200 leaf stage for tests and bench.py.  It mirrors
+the reference's operation set: ``batched_condense``,
+``leaf_solve``, ``assemble_reduced``, with ParameterError / ResonanceError as in
+proj/include/hps/errors.hpp:10-26.  There is no CPU fallback: if the CUDA
+library is missing or no GPU is visible the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libhps_leaf_b200.so")
+
+HPS_OK, HPS_ERR_RESONANCE, HPS_ERR_PARAM, HPS_ERR_CUDA = 0, 1, 2, 3
+STORAGE_RECOMPUTE, STORAGE_STORE = 0, 1
+
+
+class ParameterError(ValueError):
+    """hps::ParameterError (errors.hpp:10-13)."""
+
+
+class ResonanceError(RuntimeError):
+    """hps::ResonanceError(element_id) (errors.hpp:18-26)."""
+
+    def __init__(self, element_id, msg, failing=()):
+        super().__init__(msg)
+        self.element_id = element_id
+        self.failing = list(failing)
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+class _Desc(C.Structure):
+    _fields_ = [("p", C.c_int32), ("nx", C.c_int32), ("ny", C.c_int32), ("storage", C.c_int32),
+                ("a", C.c_double), ("kappa", C.c_double), ("workspace_bytes", C.c_int64)]
+
+
+class _Info(C.Structure):
+    _fields_ = [("p", C.c_int32), ("n_i", C.c_int32), ("n_b", C.c_int32), ("n_leaves", C.c_int32),
+                ("chunk_leaves", C.c_int32), ("resident_ctas", C.c_int32),
+                ("workspace_bytes_per_leaf", C.c_int64), ("n_active", C.c_int64), ("N", C.c_int64)]
+
+
+class _Timing(C.Structure):
+    _fields_ = [("ms_total", C.c_float), ("ms_assemble", C.c_float), ("ms_lu_schur", C.c_float),
+                ("ms_scatter", C.c_float), ("kernels", C.c_int32), ("chunks", C.c_int32)]
+
+
+_lib = None
+EXPORTED = ["hps_gpu_create", "hps_gpu_destroy", "hps_gpu_last_error", "hps_gpu_get_info",
+            "hps_gpu_get_timing", "hps_gpu_condense", "hps_gpu_condense_device", "hps_gpu_leaf_solve",
+            "hps_gpu_reduced_pattern", "hps_gpu_assemble_reduced", "hps_gpu_assemble_reduced_device",
+            "hps_gpu_set_fault_injection", "hps_host_alloc", "hps_host_free", "hps_gpu_version"]
+
+
+def lib():
+    """Load libhps_leaf_b200.so (fails loudly when the CUDA build is missing)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        L.hps_gpu_last_error.restype = C.c_char_p
+        L.hps_gpu_last_error.argtypes = [C.c_void_p]
+        L.hps_gpu_version.restype = C.c_char_p
+        L.hps_gpu_create.argtypes = [C.c_int, C.POINTER(_Desc), C.POINTER(C.c_void_p)]
+        L.hps_gpu_destroy.argtypes = [C.c_void_p]
+        L.hps_host_alloc.restype = C.c_void_p
+        L.hps_host_alloc.argtypes = [C.c_size_t]
+        L.hps_host_free.argtypes = [C.c_void_p]
+        for name in ("hps_gpu_condense", "hps_gpu_condense_device", "hps_gpu_leaf_solve",
+                     "hps_gpu_reduced_pattern", "hps_gpu_assemble_reduced",
+                     "hps_gpu_assemble_reduced_device", "hps_gpu_set_fault_injection",
+                     "hps_gpu_get_info", "hps_gpu_get_timing"):
+            getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def _f64(a, shape=None):
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    if shape is not None:
+        a = a.reshape(shape)
+    return a
+
+
+class LeafStage:
+    """One GPU context (hps_gpu_ctx) for an nx x ny mesh of p x p leaves."""
+
+    def __init__(self, p, nx, ny, kappa, a=None, storage=STORAGE_RECOMPUTE, device=0,
+                 workspace_bytes=0):
+        L = lib()
+        d = _Desc(p=p, nx=nx, ny=ny, storage=storage, a=(1.0 / nx if a is None else a),
+                  kappa=kappa, workspace_bytes=int(workspace_bytes))
+        h = C.c_void_p()
+        rc = L.hps_gpu_create(device, C.byref(d), C.byref(h))
+        if rc != HPS_OK:
+            msg = L.hps_gpu_last_error(None).decode()
+            raise (ParameterError if rc == HPS_ERR_PARAM else CudaError)(msg)
+        self._h = h
+        self.p, self.nx, self.ny, self.kappa = p, nx, ny, kappa
+        self.n_leaves = nx * ny
+        self.n_i, self.n_b = (p - 2) ** 2, 4 * (p - 1)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hps_gpu_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # -- errors -------------------------------------------------------------------------------
+    def _check(self, rc, status=None, e0=0):
+        if rc == HPS_OK:
+            return
+        msg = lib().hps_gpu_last_error(self._h).decode()
+        if rc == HPS_ERR_RESONANCE:
+            failing = [] if status is None else [e0 + int(i) for i in np.nonzero(status)[0]]
+            raise ResonanceError(failing[0] if failing else -1, msg, failing)
+        if rc == HPS_ERR_PARAM:
+            raise ParameterError(msg)
+        raise CudaError(msg)
+
+    # -- info ---------------------------------------------------------------------------------
+    def info(self):
+        i = _Info()
+        self._check(lib().hps_gpu_get_info(self._h, C.byref(i)))
+        return {k: getattr(i, k) for k, _ in _Info._fields_}
+
+    def timing(self):
+        t = _Timing()
+        self._check(lib().hps_gpu_get_timing(self._h, C.byref(t)))
+        return {k: getattr(t, k) for k, _ in _Timing._fields_}
+
+    def set_fault_injection(self, elements):
+        el = np.asarray(elements, np.int32)
+        self._check(lib().hps_gpu_set_fault_injection(self._h, _ptr(el), el.size))
+
+    # -- batched_condense ---------------------------------------------------------------------
+    def condense(self, b, f, e0=0, out=None, raise_on_resonance=True):
+        """b, f: (n, p*p) host arrays for elements [e0, e0+n).  Returns (T, w, status)."""
+        pp = self.p * self.p
+        b = _f64(b, (-1, pp)); f = _f64(f, (-1, pp))
+        n = b.shape[0]
+        if out is None:
+            T = np.empty((n, self.n_b, self.n_b)); w = np.empty((n, self.n_b))
+        else:
+            T, w = out
+        st = np.zeros(n, np.int32)
+        rc = lib().hps_gpu_condense(self._h, e0, e0 + n, _ptr(b), _ptr(f), _ptr(T), _ptr(w), None, _ptr(st))
+        if rc != HPS_OK and (rc != HPS_ERR_RESONANCE or raise_on_resonance):
+            self._check(rc, st, e0)
+        return T, w, st
+
+    def condense_device(self, e0, n, d_b, d_f, d_T, d_w, d_status, stream=0):
+        """Device-resident variant: arguments are raw device pointers (ints)."""
+        rc = lib().hps_gpu_condense_device(self._h, e0, n, C.c_void_p(d_b), C.c_void_p(d_f), C.c_void_p(d_T),
+                                           C.c_void_p(d_w), C.c_void_p(d_status), C.c_void_p(stream))
+        self._check(rc)
+
+    # -- leaf_solve ---------------------------------------------------------------------------
+    def leaf_solve(self, b, f, v, e0=0):
+        pp = self.p * self.p
+        b = _f64(b, (-1, pp)); f = _f64(f, (-1, pp)); v = _f64(v, (-1, self.n_b))
+        n = b.shape[0]
+        u = np.empty((n, pp)); st = np.zeros(n, np.int32)
+        rc = lib().hps_gpu_leaf_solve(self._h, e0, e0 + n, _ptr(b), _ptr(f), _ptr(v), _ptr(u), _ptr(st))
+        self._check(rc, st, e0)
+        return u
+
+    # -- assemble_reduced ---------------------------------------------------------------------
+    def reduced_pattern(self):
+        nnz = C.c_int64()
+        self._check(lib().hps_gpu_reduced_pattern(self._h, C.byref(nnz), None, None))
+        na = self.info()["n_active"]
+        rp = np.empty(na + 1, np.int64); ci = np.empty(max(nnz.value, 1), np.int32)
+        self._check(lib().hps_gpu_reduced_pattern(self._h, C.byref(nnz), _ptr(rp), _ptr(ci)))
+        return rp, ci[:nnz.value]
+
+    def assemble_reduced(self, T, w, g_bnd):
+        rp, ci = self.reduced_pattern()
+        T = _f64(T); w = _f64(w); g_bnd = _f64(g_bnd)
+        vals = np.empty(ci.size); rhs = np.empty(rp.size - 1)
+        self._check(lib().hps_gpu_assemble_reduced(self._h, _ptr(T), _ptr(w), _ptr(g_bnd), _ptr(vals), _ptr(rhs)))
+        return rp, ci, vals, rhs
+
+
+class PinnedArray:
+    """Page-locked host array from hps_host_alloc (for overlapped H2D/D2H)."""
+
+    def __init__(self, shape, dtype=np.float64):
+        n = int(np.prod(shape)) * np.dtype(dtype).itemsize
+        self._p = lib().hps_host_alloc(max(n, 1))
+        if not self._p:
+            raise CudaError("hps_host_alloc failed")
+        buf = (C.c_char * max(n, 1)).from_address(self._p)
+        self.array = np.frombuffer(buf, dtype=dtype, count=int(np.prod(shape))).reshape(shape)
+
+    def free(self):
+        if self._p:
+            self.array = None
+            lib().hps_host_free(C.c_void_p(self._p))
+            self._p = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass

@@ -67,7 +67,7 @@ typedef struct {
   int64_t N;               /* global DOF */
 } hps_gpu_info_t;
 
-/* Device-side timing of the last call, CUDA events on the compute stream. */
+/* Device-side timing (CUDA events on the launching stream). */
 typedef struct {
   float ms_total;          /* first kernel start -> last kernel end */
   float ms_assemble;       /* K1, summed over chunks */
@@ -82,7 +82,11 @@ int hps_gpu_create(int device, const hps_leaf_desc* desc, hps_gpu_ctx** out);
 void hps_gpu_destroy(hps_gpu_ctx* ctx);
 const char* hps_gpu_last_error(const hps_gpu_ctx* ctx);
 int hps_gpu_get_info(const hps_gpu_ctx* ctx, hps_gpu_info_t* out);
-int hps_gpu_get_timing(const hps_gpu_ctx* ctx, hps_gpu_timing_t* out);
+/* Device time of the kernels enqueued since the last reset (host-buffer calls
+ * reset on entry; device-resident calls accumulate).  Synchronizes on the last
+ * recorded event. */
+int hps_gpu_get_timing(hps_gpu_ctx* ctx, hps_gpu_timing_t* out);
+int hps_gpu_reset_timing(hps_gpu_ctx* ctx);
 
 /* batched_condense (per leaf condense_leaf :279-287) for
  * elements [e0, e1).  Inputs b, f are the (e1-e0) leaves' samples (host).

@@ -200,7 +200,10 @@ struct hps_gpu_ctx {
   DevBuf m_elem_edges, m_edge_elems, m_edge_sides, m_edge_cols, m_edge_ne, m_edge_off;
   cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_in_ready[2]{}, ev_in_free[2]{}, ev_out_ready[2]{}, ev_out_free[2]{};
-  std::vector<cudaEvent_t> tev;  // timing events (3 per chunk) on the compute stream
+  std::vector<cudaEvent_t> tev;  // timing events, 3 per chunk (before K1, K1|K2, after K2)
+  int tslots = 0;                // chunk triplets recorded since the last reset
+  int tkernels = 0;              // kernels launched since the last reset
+  float ms_scatter = 0.0f;
   hps_gpu_timing_t timing{};
   bool has_inject = false;
   int store_e0 = -1, store_e1 = -1;
@@ -276,29 +279,41 @@ int resonance_error(hps_gpu_ctx* ctx, const std::vector<int>& bad) {
                        id_list(bad) + "]");
 }
 
-void finish_timing(hps_gpu_ctx* ctx, int nchunks, int kernels_per_chunk) {
+void reset_timing(hps_gpu_ctx* ctx) {
+  ctx->tslots = 0;
+  ctx->tkernels = 0;
+  ctx->ms_scatter = 0.0f;
+}
+
+// Sum the per-chunk CUDA-event intervals recorded since the last reset.
+void finish_timing(hps_gpu_ctx* ctx) {
   hps_gpu_timing_t t{};
-  t.chunks = nchunks;
-  t.kernels = nchunks * kernels_per_chunk;
-  if (nchunks > 0) {
-    cudaEventSynchronize(ctx->tev[3 * nchunks - 1]);
-    for (int c = 0; c < nchunks; ++c) {
+  const int n = ctx->tslots;
+  t.chunks = n;
+  t.kernels = ctx->tkernels;
+  t.ms_scatter = ctx->ms_scatter;
+  if (n > 0) {
+    cudaEventSynchronize(ctx->tev[3 * n - 1]);
+    for (int c = 0; c < n; ++c) {
       float a = 0, b = 0;
       cudaEventElapsedTime(&a, ctx->tev[3 * c], ctx->tev[3 * c + 1]);
       cudaEventElapsedTime(&b, ctx->tev[3 * c + 1], ctx->tev[3 * c + 2]);
       t.ms_assemble += a;
       t.ms_lu_schur += b;
     }
-    cudaEventElapsedTime(&t.ms_total, ctx->tev[0], ctx->tev[3 * nchunks - 1]);
+    cudaEventElapsedTime(&t.ms_total, ctx->tev[0], ctx->tev[3 * n - 1]);
   }
+  t.ms_total += t.ms_scatter;
   ctx->timing = t;
 }
 
 // Device pipeline for one chunk of `n` leaves starting at element e (K1 + K2).
 void enqueue_condense_chunk(hps_gpu_ctx* ctx, int e, int n, const double* d_b, const double* d_f,
-                            double* d_T, double* d_w, int* d_status, cudaStream_t st, int ci) {
+                            double* d_T, double* d_w, int* d_status, cudaStream_t st) {
   const LeafDims& d = ctx->d;
   const int* inj = ctx->has_inject ? ctx->inject_all.as<int>() + e : nullptr;
+  const int ci = ctx->tslots++;
+  ctx->tkernels += 3;
   cudaEventRecord(ctx->timing_event(3 * ci), st);
   hpsg::launch_assemble(d, ctx->rowcode.as<int>(), ctx->colcode.as<int>(), ctx->Ds.as<double>(),
                         ctx->D2.as<double>(), ctx->k2, d_b, d_f, ctx->ws.as<double>(),
@@ -475,9 +490,17 @@ int hps_gpu_get_info(const hps_gpu_ctx* ctx, hps_gpu_info_t* out) {
   return HPS_OK;
 }
 
-int hps_gpu_get_timing(const hps_gpu_ctx* ctx, hps_gpu_timing_t* out) {
+int hps_gpu_get_timing(hps_gpu_ctx* ctx, hps_gpu_timing_t* out) {
   if (!ctx || !out) return HPS_ERR_PARAM;
+  cudaSetDevice(ctx->device);
+  finish_timing(ctx);
   *out = ctx->timing;
+  return HPS_OK;
+}
+
+int hps_gpu_reset_timing(hps_gpu_ctx* ctx) {
+  if (!ctx) return HPS_ERR_PARAM;
+  reset_timing(ctx);
   return HPS_OK;
 }
 
@@ -518,6 +541,7 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
     CK(ctx->out_w[i].ensure(size_t(chunk) * d.nb * 8));
     CK(ctx->out_st[i].ensure(size_t(chunk) * 4));
   }
+  reset_timing(ctx);
   int ci = 0;
   for (int c0 = e0; c0 < e1; c0 += chunk, ++ci) {
     const int n = std::min(chunk, e1 - c0);
@@ -531,7 +555,7 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
     CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_out_free[k], 0));
     enqueue_condense_chunk(ctx, c0, n, ctx->in_b[k].as<double>(), ctx->in_f[k].as<double>(),
                            ctx->out_T[k].as<double>(), ctx->out_w[k].as<double>(),
-                           ctx->out_st[k].as<int>(), ctx->s_comp, ci);
+                           ctx->out_st[k].as<int>(), ctx->s_comp);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev_in_free[k], ctx->s_comp));
     CK(cudaEventRecord(ctx->ev_out_ready[k], ctx->s_comp));
@@ -544,7 +568,7 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
   }
   CK(cudaStreamSynchronize(ctx->s_d2h));
   CK(cudaStreamSynchronize(ctx->s_comp));
-  finish_timing(ctx, ci, 3);
+  finish_timing(ctx);
   if (ctx->desc.storage == HPS_STORAGE_STORE) {
     ctx->store_e0 = e0;
     ctx->store_e1 = e1;
@@ -569,12 +593,9 @@ int hps_gpu_condense_device(hps_gpu_ctx* ctx, int32_t e0, int32_t n, const doubl
   for (int c0 = 0; c0 < n; c0 += ctx->chunk, ++ci) {
     const int m = std::min(ctx->chunk, n - c0);
     enqueue_condense_chunk(ctx, e0 + c0, m, d_b + c0 * pp, d_f + c0 * pp, d_T + c0 * nb2,
-                           d_w + size_t(c0) * d.nb, d_status + c0, st, ci);
+                           d_w + size_t(c0) * d.nb, d_status + c0, st);
     CK(cudaGetLastError());
   }
-  ctx->timing = hps_gpu_timing_t{};
-  ctx->timing.chunks = ci;
-  ctx->timing.kernels = 3 * ci;
   return HPS_OK;
 }
 
@@ -598,6 +619,7 @@ int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b
     CK(ctx->out_u[i].ensure(size_t(chunk) * pp * 8));
     CK(ctx->out_st[i].ensure(size_t(chunk) * 4));
   }
+  reset_timing(ctx);
   int ci = 0;
   for (int c0 = e0; c0 < e1; c0 += chunk, ++ci) {
     const int n = std::min(chunk, e1 - c0);
@@ -611,7 +633,9 @@ int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b
     CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_in_ready[k], 0));
     CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_out_free[k], 0));
     cudaStream_t st = ctx->s_comp;
-    cudaEventRecord(ctx->timing_event(3 * ci), st);
+    const int slot = ctx->tslots++;
+    ctx->tkernels += store ? 3 : 4;
+    cudaEventRecord(ctx->timing_event(3 * slot), st);
     hpsg::LuArgs a;
     a.ws = ctx->ws.as<double>();
     a.linv = ctx->linv.as<double>();
@@ -644,12 +668,12 @@ int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b
                                   ctx->in_v[k].as<double>(), a.ws, ctx->norms.as<double>(), inj, n, st);
       a.factor = 1;
     }
-    cudaEventRecord(ctx->timing_event(3 * ci + 1), st);
+    cudaEventRecord(ctx->timing_event(3 * slot + 1), st);
     a.d = dsolve;
     hpsg::launch_lu_schur(a, n, st);
     hpsg::launch_backsolve(dsolve, a.ws, a.perm, ctx->in_v[k].as<double>(), ctx->out_u[k].as<double>(),
                            n, st);
-    cudaEventRecord(ctx->timing_event(3 * ci + 2), st);
+    cudaEventRecord(ctx->timing_event(3 * slot + 2), st);
     CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev_in_free[k], st));
     CK(cudaEventRecord(ctx->ev_out_ready[k], st));
@@ -660,7 +684,7 @@ int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b
   }
   CK(cudaStreamSynchronize(ctx->s_d2h));
   CK(cudaStreamSynchronize(ctx->s_comp));
-  finish_timing(ctx, ci, store ? 3 : 4);
+  finish_timing(ctx);
   std::vector<int> bad;
   for (int i = 0; i < e1 - e0; ++i)
     if (status[i]) bad.push_back(e0 + i);
@@ -720,7 +744,10 @@ int hps_gpu_assemble_reduced(hps_gpu_ctx* ctx, const double* T, const double* w,
   CK(cudaMemcpyAsync(dT.ptr, T, nl * nb * nb * 8, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(dw.ptr, w, nl * nb * 8, cudaMemcpyHostToDevice, st));
   CK(cudaMemcpyAsync(dg.ptr, g_bnd, ng * 8, cudaMemcpyHostToDevice, st));
-  cudaEvent_t t0 = ctx->timing_event(0), t1 = ctx->timing_event(1);
+  reset_timing(ctx);
+  cudaEvent_t t0, t1;
+  CK(cudaEventCreate(&t0));
+  CK(cudaEventCreate(&t1));
   cudaEventRecord(t0, st);
   hpsg::launch_reduced_values(ctx->mesh_dev(), dT.as<double>(), dw.as<double>(), dg.as<double>(),
                               dv.as<double>(), dr.as<double>(), st);
@@ -729,11 +756,11 @@ int hps_gpu_assemble_reduced(hps_gpu_ctx* ctx, const double* T, const double* w,
   CK(cudaMemcpyAsync(values, dv.ptr, size_t(nnz) * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(rhs, dr.ptr, size_t(na) * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  hps_gpu_timing_t t{};
-  cudaEventElapsedTime(&t.ms_scatter, t0, t1);
-  t.ms_total = t.ms_scatter;
-  t.kernels = 1;
-  ctx->timing = t;
+  cudaEventElapsedTime(&ctx->ms_scatter, t0, t1);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  ctx->tkernels = 1;
+  finish_timing(ctx);
   return HPS_OK;
 }
 

@@ -388,7 +388,10 @@ __global__ void __launch_bounds__(NT, 2) k2_lu_schur_kernel(LuArgs a) {
   L.sm = sm;
   double* Linv = a.linv + (size_t)leaf * d.nblk * 4096;
   short* perm_g = a.perm + (size_t)leaf * d.Rpad;
-  for (int i = threadIdx.x; i < d.Rpad; i += NT) sm->perm[i] = a.factor ? (short)i : perm_g[i];
+  // Entries past Rpad are read by masked-out tile rows (e.g. the D-row tiles start at ni, which
+  // need not be 64-aligned): point them at a valid row so the gathers stay in bounds.
+  for (int i = threadIdx.x; i < MAX_RPAD; i += NT)
+    sm->perm[i] = i < d.Rpad ? (a.factor ? (short)i : perm_g[i]) : (short)(d.Rpad - 1);
   __syncthreads();
   double minpiv = INFINITY;  // meaningful on thread 0
 

@@ -55,7 +55,7 @@ class _Timing(C.Structure):
 
 _lib = None
 EXPORTED = ["hps_gpu_create", "hps_gpu_destroy", "hps_gpu_last_error", "hps_gpu_get_info",
-            "hps_gpu_get_timing", "hps_gpu_condense", "hps_gpu_condense_device", "hps_gpu_leaf_solve",
+            "hps_gpu_get_timing", "hps_gpu_reset_timing", "hps_gpu_condense", "hps_gpu_condense_device", "hps_gpu_leaf_solve",
             "hps_gpu_reduced_pattern", "hps_gpu_assemble_reduced", "hps_gpu_assemble_reduced_device",
             "hps_gpu_set_fault_injection", "hps_host_alloc", "hps_host_free", "hps_gpu_version"]
 
@@ -78,7 +78,7 @@ def lib():
         for name in ("hps_gpu_condense", "hps_gpu_condense_device", "hps_gpu_leaf_solve",
                      "hps_gpu_reduced_pattern", "hps_gpu_assemble_reduced",
                      "hps_gpu_assemble_reduced_device", "hps_gpu_set_fault_injection",
-                     "hps_gpu_get_info", "hps_gpu_get_timing"):
+                     "hps_gpu_get_info", "hps_gpu_get_timing", "hps_gpu_reset_timing"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -152,6 +152,9 @@ class LeafStage:
         t = _Timing()
         self._check(lib().hps_gpu_get_timing(self._h, C.byref(t)))
         return {k: getattr(t, k) for k, _ in _Timing._fields_}
+
+    def reset_timing(self):
+        self._check(lib().hps_gpu_reset_timing(self._h))
 
     def set_fault_injection(self, elements):
         el = np.asarray(elements, np.int32)

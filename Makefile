@@ -25,7 +25,7 @@ $(OBJDIR)/%.cpp.o: $(SRC)/%.cpp $(HDRS)
 
 $(LIB): $(OBJS)
 	@mkdir -p $(dir $@)
-	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -lcudart
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS)
 
 oracle:
 	$(MAKE) -s -C oracle
@@ -34,4 +34,12 @@ clean:
 	rm -rf build $(LIB)
 	$(MAKE) -s -C oracle clean
 
-.PHONY: all oracle clean
+.PHONY: all oracle clean cxx_test
+
+CXX_TEST := build/test_leaf_api
+cxx_test: $(CXX_TEST)
+
+$(CXX_TEST): tests/cxx/test_leaf_api.cpp include/hps/leaf_gpu.hpp include/hps_leaf_gpu.h $(LIB)
+	@mkdir -p build
+	g++ -std=c++20 -O2 -Iinclude -o $@ $< -L$(dir $(LIB)) -lhps_leaf_b200 \
+	    -Wl,-rpath,'$$ORIGIN/../paper_2211_14969_b200/_lib'

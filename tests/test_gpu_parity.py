@@ -1,0 +1,245 @@
+"""GPU parity tests: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bars (BASELINE.json north star): Schur complements T_flux within relative
+Frobenius 1e-10 per leaf, interface indices bit-exact, final PDE solution within
+1e-9 relative.  Also: bitwise determinism across chunking / leaf ranges
+(parallel.hpp:21-22), store == recompute bitwise,
+resonance error reporting (errors.hpp:18-26).
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import pyoracle as O
+from paper_2211_14969_b200 import problems as P
+import hps_harness as H
+
+pytestmark = pytest.mark.gpu
+
+TOL_T = 1e-10      # relative Frobenius per leaf (north star)
+TOL_U = 1e-9       # final solution (north star)
+
+
+def G():
+    from paper_2211_14969_b200 import leaf_gpu
+    return leaf_gpu
+
+
+def rel_fro(a, b):
+    num = np.linalg.norm((a - b).reshape(a.shape[0], -1), axis=1)
+    den = np.linalg.norm(b.reshape(b.shape[0], -1), axis=1)
+    return num / np.maximum(den, 1e-300)
+
+
+def random_leaves(p, n, seed, lo=0.0, hi=1.0):
+    rng = np.random.default_rng(seed)
+    return rng.uniform(lo, hi, (n, p * p)), rng.uniform(-1, 1, (n, p * p))
+
+
+@pytest.mark.parametrize("p,kappa,n", [(4, 2.0, 5), (5, 3.0, 4), (6, 7.0, 6), (8, 10.0, 9), (12, 20.0, 7),
+                                       (13, 15.0, 3), (16, 40.0, 5), (22, 100.0, 6), (27, 80.0, 3),
+                                       (32, 250.0, 3), (37, 300.0, 2), (42, 500.0, 3)])
+def test_condense_parity_random(p, kappa, n):
+    b, f = random_leaves(p, n, seed=p)
+    a = 1.0 / max(n, 2)
+    ref = O.batched_condense(p, a, kappa, b, f)
+    with G().LeafStage(p, n, 1, kappa, a=a) as st:
+        T, w, s = st.condense(b, f)
+    assert not s.any()
+    eT = rel_fro(T, ref["T"])
+    ew = rel_fro(w, ref["w"])
+    assert eT.max() <= TOL_T, eT
+    assert ew.max() <= TOL_T, ew
+
+
+def test_c1_fixtures_parity_and_solution():
+    """C1 (p=12, 16x16, Poisson, b=1) with the SURVEY §8d fixtures: f = 2pi^2 sin(pi x) sin(pi y)
+    (exact u = sin sin, g = 0) and f ~ U(-1,1) seed 0."""
+    cfg = P.config("C1")
+    p, nx, ny = cfg["p"], cfg["nx"], cfg["ny"]
+    X, Y = P.leaf_coords(nx, ny, p)
+    b = np.ones_like(X)
+    f1 = 2 * math.pi ** 2 * np.sin(math.pi * X) * np.sin(math.pi * Y)
+    f2 = np.random.default_rng(0).uniform(-1, 1, X.shape)
+    gb = P.boundary_samples(nx, ny, p, lambda x, y: 0 * x)
+    with G().LeafStage(p, nx, ny, 0.0) as st:
+        for f in (f1, f2):
+            ref = O.batched_condense(p, cfg["a"], 0.0, b, f)
+            T, w, s = st.condense(b, f)
+            assert rel_fro(T, ref["T"]).max() <= TOL_T
+            assert rel_fro(w, ref["w"]).max() <= TOL_T
+        # end to end with the GPU leaf stage vs the oracle pipeline, and vs the exact solution
+        gpu = lambda bb, ff: st.condense(bb, ff)[:2]
+        u_g, _ = H.hps_pipeline(nx, ny, p, 0.0, b, f1, gb, condense=gpu,
+                                leaf_solve=lambda bb, ff, vv: st.leaf_solve(bb, ff, vv),
+                                assemble=lambda T, w, g: st.assemble_reduced(T, w, g))
+    u_o, _ = H.hps_pipeline(nx, ny, p, 0.0, b, f1, gb)
+    cls = H.classify(nx, ny, p)
+    m = cls != 3
+    assert np.max(np.abs(u_g[m] - u_o[m])) / np.max(np.abs(u_o[m])) <= TOL_U
+    GX, GY = H.global_coords(nx, ny, p)
+    exact = np.sin(math.pi * GX) * np.sin(math.pi * GY)
+    assert np.max(np.abs(u_g[m] - exact[m])) <= 1e-8
+
+
+@pytest.mark.parametrize("nx,ny,p", [(1, 1, 6), (2, 2, 4), (2, 2, 8), (3, 4, 6), (5, 3, 12), (16, 16, 12),
+                                     (7, 9, 22), (12, 10, 42)])
+def test_reduced_pattern_bit_exact(nx, ny, p):
+    with G().LeafStage(p, nx, ny, 1.0) as st:
+        rp, ci = st.reduced_pattern()
+    if nx * ny == 1:
+        assert rp.size == 1 and ci.size == 0
+        return
+    rpo, cio = O.reduced_pattern(nx, ny, p)
+    assert rp.dtype == np.int64 and ci.dtype == np.int32
+    assert np.array_equal(rp, rpo)
+    assert np.array_equal(ci, cio)
+
+
+@pytest.mark.parametrize("nx,ny,p", [(2, 2, 8), (3, 5, 10), (6, 4, 12)])
+def test_reduced_values_bit_exact_given_T(nx, ny, p):
+    """K4 scatter reproduces the oracle's assemble_reduced bit for bit on the same T, w, g."""
+    rng = np.random.default_rng(11)
+    nb = 4 * (p - 1)
+    T = rng.standard_normal((nx * ny, nb, nb)); w = rng.standard_normal((nx * ny, nb))
+    gb = P.boundary_samples(nx, ny, p, lambda x, y: np.cos(3 * x) + y * y)
+    rpo, cio, vo, ro = O.assemble_reduced(nx, ny, p, T, w, gb)
+    with G().LeafStage(p, nx, ny, 1.0) as st:
+        rp, ci, v, r = st.assemble_reduced(T, w, gb)
+    assert np.array_equal(rp, rpo) and np.array_equal(ci, cio)
+    assert np.array_equal(v.view(np.int64), vo.view(np.int64))
+    assert np.array_equal(r.view(np.int64), ro.view(np.int64))
+
+
+@pytest.mark.parametrize("p,kappa", [(8, 5.0), (12, 20.0), (22, 100.0), (27, 60.0)])
+def test_leaf_solve_parity_and_store_equals_recompute(p, kappa):
+    n = 5
+    b, f = random_leaves(p, n, seed=100 + p)
+    v = np.random.default_rng(7).uniform(-1, 1, (n, 4 * (p - 1)))
+    a = 0.2
+    uo = O.batched_leaf_solve(p, a, kappa, b, f, v)
+    with G().LeafStage(p, n, 1, kappa, a=a) as st:
+        ur = st.leaf_solve(b, f, v)
+    assert rel_fro(ur, uo).max() <= TOL_T
+    with G().LeafStage(p, n, 1, kappa, a=a, storage=G().STORAGE_STORE) as st:
+        st.condense(b, f)
+        us = st.leaf_solve(b, f, v)
+        us2 = st.leaf_solve(b, f, v)            # repeated solves on kept factors
+    assert np.array_equal(ur.view(np.int64), us.view(np.int64))
+    assert np.array_equal(us.view(np.int64), us2.view(np.int64))
+
+
+def test_bitwise_independent_of_chunking_and_range():
+    """Results do not depend on chunk size, leaf range or batch position."""
+    p, nx, ny, kappa = 22, 6, 5, 100.0
+    X, Y = P.leaf_coords(nx, ny, p)
+    b = P.crystal_field(X, Y); f = np.sin(X) * np.cos(Y)
+    with G().LeafStage(p, nx, ny, kappa) as st:
+        T1, w1, _ = st.condense(b, f)
+    with G().LeafStage(p, nx, ny, kappa, workspace_bytes=7 * 3_000_000) as st:   # tiny chunks
+        assert st.info()["chunk_leaves"] < nx * ny
+        T2, w2, _ = st.condense(b, f)
+        T3, w3, _ = st.condense(b[11:23], f[11:23], e0=11)
+    assert np.array_equal(T1.view(np.int64), T2.view(np.int64))
+    assert np.array_equal(w1.view(np.int64), w2.view(np.int64))
+    assert np.array_equal(T1[11:23].view(np.int64), T3.view(np.int64))
+
+
+def test_resonance_error_reports_smallest_element():
+    p, nx, ny = 10, 4, 3
+    b, f = random_leaves(p, nx * ny, seed=5)
+    with G().LeafStage(p, nx, ny, 3.0) as st:
+        st.set_fault_injection([9, 4, 7])
+        with pytest.raises(G().ResonanceError) as ei:
+            st.condense(b, f)
+        assert ei.value.element_id == 4
+        assert ei.value.failing == [4, 7, 9]
+        assert "element 4" in str(ei.value) and "4,7,9" in str(ei.value)
+        T, w, s = st.condense(b, f, raise_on_resonance=False)
+        assert list(np.nonzero(s)[0]) == [4, 7, 9]
+        # the same injection in the oracle agrees
+        r = O.batched_condense(p, 1.0 / nx, 3.0, b, f, inject=[9, 4, 7], raise_on_resonance=False)
+        assert list(np.nonzero(r["status"])[0]) == [4, 7, 9]
+        ok = s == 0
+        assert rel_fro(T[ok], r["T"][ok]).max() <= TOL_T
+        st.set_fault_injection([])
+        st.condense(b, f)
+        with pytest.raises(G().ResonanceError):
+            st.set_fault_injection([2])
+            st.leaf_solve(b, f, np.zeros((nx * ny, 4 * (p - 1))))
+
+
+def test_parameter_errors():
+    with pytest.raises(G().ParameterError):
+        G().LeafStage(3, 2, 2, 1.0)
+    with pytest.raises(G().ParameterError):
+        G().LeafStage(8, 2, 2, 1.0, a=0.0)
+    with pytest.raises(G().ParameterError):
+        G().LeafStage(8, 2, 2, -1.0)
+    with G().LeafStage(8, 2, 2, 1.0) as st:
+        b, f = random_leaves(8, 5, 0)
+        with pytest.raises(G().ParameterError):
+            st.condense(b, f)        # 5 leaves on a 4-leaf mesh
+
+
+@pytest.mark.parametrize("n", [2, 4])
+@pytest.mark.parametrize("p", [6, 10])
+@pytest.mark.parametrize("kappa", [0.0, 2 * math.pi])
+def test_pipeline_matches_dense_global_solve(n, p, kappa):
+    """Acceptance 1 with the GPU leaf stage."""
+    nx = ny = n
+    ut = P.analytic_j0(max(kappa, 1.0))
+    _, _, b, f = H.leaf_inputs(nx, ny, p, lambda x, y: 1.0 + 0 * x, lambda x, y: np.sin(3 * x) * np.cos(2 * y))
+    gb = P.boundary_samples(nx, ny, p, ut)
+    with G().LeafStage(p, nx, ny, kappa) as st:
+        u, _ = H.hps_pipeline(nx, ny, p, kappa, b, f, gb, condense=lambda bb, ff: st.condense(bb, ff)[:2],
+                              leaf_solve=lambda bb, ff, vv: st.leaf_solve(bb, ff, vv),
+                              assemble=lambda T, w, g: st.assemble_reduced(T, w, g))
+    A, rhs, cls = H.assemble_global_dense(nx, ny, p, kappa, b, f, gb)
+    ud = np.linalg.solve(A, rhs)
+    m = cls != 3
+    assert np.max(np.abs(u[m] - ud[m])) / np.max(np.abs(ud[m])) <= TOL_U
+
+
+def test_c2_full_scale():
+    """C2 (p=22, 48x48, kappa=100, crystal b) at full size: no resonance flags, a seeded
+    subset of leaves matches the oracle, two runs are bitwise identical, and the constant
+    field is annihilated on non-corner rows where b is irrelevant (kappa-free check below)."""
+    cfg = P.config("C2")
+    p, nx, ny = cfg["p"], cfg["nx"], cfg["ny"]
+    X, Y = P.leaf_coords(nx, ny, p)
+    b = P.crystal_field(X, Y)
+    f = np.random.default_rng(2).uniform(-1, 1, X.shape)
+    with G().LeafStage(p, nx, ny, cfg["kappa"]) as st:
+        T, w, s = st.condense(b, f)
+        T2, w2, _ = st.condense(b, f)
+    assert not s.any()
+    assert np.array_equal(T.view(np.int64), T2.view(np.int64))
+    idx = np.random.default_rng(3).choice(nx * ny, 24, replace=False)
+    ref = O.batched_condense(p, cfg["a"], cfg["kappa"], b[idx], f[idx])
+    assert rel_fro(T[idx], ref["T"]).max() <= TOL_T
+    assert rel_fro(w[idx], ref["w"]).max() <= TOL_T
+
+
+def test_c4_subset_and_laplace_property():
+    """C4 shapes (p=42, kappa=500, crystal b): a leaf subset vs the oracle; at kappa=0 the
+    DtN map annihilates constants on non-corner rows for every leaf of a 16x16 mesh."""
+    cfg = P.config("C4")
+    p = cfg["p"]
+    el = np.array([0, 97, 4801, 9603])
+    X, Y = P.leaf_coords(cfg["nx"], cfg["ny"], p, elements=el)
+    b = P.crystal_field(X, Y); f = np.random.default_rng(4).uniform(-1, 1, X.shape)
+    ref = O.batched_condense(p, cfg["a"], cfg["kappa"], b, f)
+    with G().LeafStage(p, cfg["nx"], cfg["ny"], cfg["kappa"]) as st:
+        for i, e in enumerate(el):
+            T, w, s = st.condense(b[i:i + 1], f[i:i + 1], e0=int(e))
+            assert rel_fro(T, ref["T"][i:i + 1]).max() <= TOL_T
+            assert rel_fro(w, ref["w"][i:i + 1]).max() <= TOL_T
+    n = 16
+    Xl, Yl = P.leaf_coords(n, n, p)
+    with G().LeafStage(p, n, n, 0.0) as st:
+        T, w, s = st.condense(P.crystal_field(Xl, Yl), np.zeros_like(Xl))
+    nc = [k for k in range(4 * (p - 1)) if k not in (0, p - 1, 2 * p - 2, 2 * p - 1)]
+    flux = T @ np.ones(4 * (p - 1))
+    assert np.max(np.abs(flux[:, nc])) <= 1e-9 * np.max(np.abs(T))

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <set>
@@ -206,6 +207,12 @@ struct hps_gpu_ctx {
   float ms_scatter = 0.0f;
   hps_gpu_timing_t timing{};
   bool has_inject = false;
+  bool phase_timers = std::getenv("HPS_PHASE_TIMERS") != nullptr;
+  // K1 materialises the operator (default); HPS_FUSED=1 evaluates the tile C-inits in K2
+  // instead (first-touch assembly, no workspace writes by K1; slower in r01 measurements).
+  bool fused = std::getenv("HPS_FUSED") != nullptr;
+  long long dephase_ns = std::getenv("HPS_DEPHASE_NS") ? std::atoll(std::getenv("HPS_DEPHASE_NS")) : 0;
+  DevBuf phase_buf;
   int store_e0 = -1, store_e1 = -1;
 
   ~hps_gpu_ctx() {
@@ -313,11 +320,16 @@ void enqueue_condense_chunk(hps_gpu_ctx* ctx, int e, int n, const double* d_b, c
   const LeafDims& d = ctx->d;
   const int* inj = ctx->has_inject ? ctx->inject_all.as<int>() + e : nullptr;
   const int ci = ctx->tslots++;
-  ctx->tkernels += 3;
+  ctx->tkernels += ctx->fused ? 2 : 3;
   cudaEventRecord(ctx->timing_event(3 * ci), st);
-  hpsg::launch_assemble(d, ctx->rowcode.as<int>(), ctx->colcode.as<int>(), ctx->Ds.as<double>(),
-                        ctx->D2.as<double>(), ctx->k2, d_b, d_f, ctx->ws.as<double>(),
-                        ctx->norms.as<double>(), inj, n, st);
+  if (ctx->fused) {
+    // K1 fused into K2 (first-touch assembly): only ||A_ii|| runs as its own kernel.
+    hpsg::launch_aii_norm(d, ctx->D2.as<double>(), ctx->k2, d_b, inj, ctx->norms.as<double>(), n, st);
+  } else {
+    hpsg::launch_assemble(d, ctx->rowcode.as<int>(), ctx->colcode.as<int>(), ctx->Ds.as<double>(),
+                          ctx->D2.as<double>(), ctx->k2, d_b, d_f, ctx->ws.as<double>(),
+                          ctx->norms.as<double>(), inj, n, st);
+  }
   cudaEventRecord(ctx->timing_event(3 * ci + 1), st);
   hpsg::LuArgs a;
   a.d = d;
@@ -330,8 +342,36 @@ void enqueue_condense_chunk(hps_gpu_ctx* ctx, int e, int n, const double* d_b, c
   a.status = d_status;
   a.minratio = ctx->minratio.as<double>();
   a.factor = 1;
+  a.dephase_ns = ctx->dephase_ns;
+  a.fused = ctx->fused ? 1 : 0;
+  a.rowcode = ctx->rowcode.as<int>();
+  a.colcode = ctx->colcode.as<int>();
+  a.Ds = ctx->Ds.as<double>();
+  a.D2 = ctx->D2.as<double>();
+  a.k2 = ctx->k2;
+  a.b = d_b;
+  a.f = d_f;
+  a.inject = inj;
+  if (ctx->phase_timers) {
+    ctx->phase_buf.ensure(size_t(ctx->chunk) * 8 * sizeof(long long));
+    cudaMemsetAsync(ctx->phase_buf.ptr, 0, size_t(n) * 8 * sizeof(long long), st);
+    a.phase_cycles = ctx->phase_buf.as<long long>();
+  }
   hpsg::launch_lu_schur(a, n, st);
   cudaEventRecord(ctx->timing_event(3 * ci + 2), st);
+  if (ctx->phase_timers) {
+    std::vector<long long> h(size_t(n) * 8);
+    cudaMemcpyAsync(h.data(), ctx->phase_buf.ptr, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    double sum[8] = {0};
+    for (int i = 0; i < n; ++i)
+      for (int k = 0; k < 8; ++k) sum[k] += double(h[size_t(i) * 8 + k]);
+    std::fprintf(stderr,
+                 "[hps phase cycles/leaf] U-part %.3g  L-part %.3g  panel %.3g (strips %.3g upd-U %.3g "
+                 "upd-L %.3g)  linv %.3g  trailing %.3g\n",
+                 sum[0] / n, sum[1] / n, sum[2] / n + sum[5] / n + sum[6] / n + sum[7] / n, sum[5] / n,
+                 sum[6] / n, sum[7] / n, sum[3] / n, sum[4] / n);
+  }
 }
 
 }  // namespace
@@ -449,7 +489,8 @@ int hps_gpu_create(int device, const hps_leaf_desc* desc, hps_gpu_ctx** out) {
   c->chunk = chunk;
   {
     hps_gpu_ctx* ctx = ctxp;
-    CK(c->ws.ensure(size_t(chunk) * d.leaf_stride * 8));
+    // + 2 rows of slack: 128-wide U tiles may read up to 64 doubles past the last row.
+    CK(c->ws.ensure((size_t(chunk) * d.leaf_stride + 2 * size_t(d.ld)) * 8));
     CK(c->linv.ensure(size_t(chunk) * d.nblk * 4096 * 8));
     CK(c->perm.ensure(size_t(chunk) * d.Rpad * 2));
     CK(c->norms.ensure(size_t(chunk) * 8));
@@ -457,7 +498,7 @@ int hps_gpu_create(int device, const hps_leaf_desc* desc, hps_gpu_ctx** out) {
     CK(c->status.ensure(size_t(chunk) * 4));
     CK(c->inject_all.ensure(size_t(c->n_leaves) * 4));
     CK(cudaMemset(c->inject_all.ptr, 0, size_t(c->n_leaves) * 4));
-    CK(cudaMemset(c->ws.ptr, 0, size_t(chunk) * d.leaf_stride * 8));
+    CK(cudaMemset(c->ws.ptr, 0, (size_t(chunk) * d.leaf_stride + 2 * size_t(d.ld)) * 8));
   }
   *out = ctx.release();
   return HPS_OK;

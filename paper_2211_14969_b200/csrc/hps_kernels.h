@@ -13,6 +13,10 @@ void launch_assemble(const LeafDims& d, const int* rowcode, const int* colcode, 
                      const double* D2, double k2, const double* b, const double* f, double* ws,
                      double* norms, const int* inject, int n_leaves, cudaStream_t st);
 
+// ||A_ii||_inf only (fused-assembly condense path).
+void launch_aii_norm(const LeafDims& d, const double* D2, double k2, const double* b,
+                     const int* inject, double* norms, int n_leaves, cudaStream_t st);
+
 // K1 (leaf-solve variant): [A_ii | f_i - A_ib v] with no D rows (rows ni..Rpad zero).
 void launch_assemble_solve(const LeafDims& d, const int* rowcode, const int* colcode,
                            const double* Ds, const double* D2, double k2, const double* b,
@@ -35,6 +39,19 @@ struct LuArgs {
   int* status;          // per leaf (factor = 1)
   double* minratio;     // per leaf, nullable
   int factor;           // 1: factor A_ii then trailing columns; 0: trailing columns only
+  long long* phase_cycles = nullptr;  // optional 8 counters per leaf (profiling)
+  long long dephase_ns = 0;           // start delay of the second CTA on each SM
+  // Fused first-touch assembly (fused = 1): tile C-inits are evaluated from the
+  // operator definition instead of loaded from a K1-materialised workspace.
+  int fused = 0;
+  const int* rowcode = nullptr;
+  const int* colcode = nullptr;
+  const double* Ds = nullptr;
+  const double* D2 = nullptr;
+  double k2 = 0.0;
+  const double* b = nullptr;           // p*p per leaf
+  const double* f = nullptr;           // p*p per leaf
+  const int* inject = nullptr;         // per leaf, nullable
 };
 size_t lu_smem_bytes();
 void launch_lu_schur(const LuArgs& a, int n_leaves, cudaStream_t st);

@@ -10,53 +10,11 @@
 //  order as the CPU oracle (oracle/hps_oracle.cpp a_entry/dn_entry), so A is
 //  bit-identical to the oracle's.
 // ============================================================================
+#include "hps_assembly.cuh"
 #include "hps_device.cuh"
 #include "hps_kernels.h"
 
 namespace hpsg {
-
-// Column/row code (built on the host once per p, see hps_host.cpp):
-//   bits 0..7  : jy (or iy)      bits 8..15 : jx (or ix)
-//   bits 16..17: kind  0 interior node, 1 boundary node, 2 load column, 3 zero
-//   bits 18..19: owning edge of a boundary node (rows only)
-__device__ __forceinline__ double a_entry(int iy, int ix, int jy, int jx, int p,
-                                          const double* __restrict__ D2, double k2, double bl) {
-  if (jy == iy && jx == ix) {
-    double v = -__ldg(D2 + iy * p + iy);
-    v = __dsub_rn(v, __ldg(D2 + ix * p + ix));
-    return __dsub_rn(v, __dmul_rn(k2, bl));
-  }
-  if (jx == ix) return -__ldg(D2 + iy * p + jy);
-  if (jy == iy) return -__ldg(D2 + ix * p + jx);
-  return 0.0;
-}
-
-__device__ __forceinline__ double dn_entry(int edge, int iy, int ix, int jy, int jx, int p,
-                                           const double* __restrict__ Ds) {
-  switch (edge) {
-    case 0: return jx == ix ? -__ldg(Ds + iy * p + jy) : 0.0;   // S: -d/dy
-    case 1: return jy == iy ? __ldg(Ds + ix * p + jx) : 0.0;    // E: +d/dx
-    case 2: return jx == ix ? __ldg(Ds + iy * p + jy) : 0.0;    // N: +d/dy
-    default: return jy == iy ? -__ldg(Ds + ix * p + jx) : 0.0;  // W: -d/dx
-  }
-}
-
-__device__ __forceinline__ double aug_value(int rcode, int ccode, int p, const double* __restrict__ Ds,
-                                            const double* __restrict__ D2, double k2,
-                                            const double* __restrict__ bl,
-                                            const double* __restrict__ fl, bool zero_aii_row) {
-  const int rkind = (rcode >> 16) & 3, ckind = (ccode >> 16) & 3;
-  if (rkind == 3 || ckind == 3) return 0.0;
-  const int iy = rcode & 255, ix = (rcode >> 8) & 255;
-  const int jy = ccode & 255, jx = (ccode >> 8) & 255;
-  if (rkind == 0) {  // interior collocation row
-    if (ckind == 2) return __ldg(fl + iy * p + ix);
-    if (ckind == 0 && zero_aii_row) return 0.0;
-    return a_entry(iy, ix, jy, jx, p, D2, k2, __ldg(bl + iy * p + ix));
-  }
-  if (ckind == 2) return 0.0;  // flux row, load column
-  return dn_entry((rcode >> 18) & 3, iy, ix, jy, jx, p, Ds);
-}
 
 // grid (ceil(Rpad / kRows), n_leaves), block 256.
 constexpr int kRows = 8;
@@ -195,6 +153,12 @@ void launch_assemble(const LeafDims& d, const int* rowcode, const int* colcode, 
   if (n_leaves <= 0) return;
   dim3 grid((d.Rpad + kRows - 1) / kRows, n_leaves);
   k1_assemble_kernel<<<grid, 256, 0, st>>>(d, rowcode, colcode, Ds, D2, k2, b, f, ws, inject);
+  k1_aii_norm_kernel<<<n_leaves, 256, 0, st>>>(d, D2, k2, b, inject, norms);
+}
+
+void launch_aii_norm(const LeafDims& d, const double* D2, double k2, const double* b,
+                     const int* inject, double* norms, int n_leaves, cudaStream_t st) {
+  if (n_leaves <= 0) return;
   k1_aii_norm_kernel<<<n_leaves, 256, 0, st>>>(d, D2, k2, b, inject, norms);
 }
 

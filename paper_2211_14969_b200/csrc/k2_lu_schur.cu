@@ -26,128 +26,193 @@
 // ============================================================================
 #include <climits>
 
+#include "hps_assembly.cuh"
 #include "hps_device.cuh"
 #include "hps_kernels.h"
 
 namespace hpsg {
 
-constexpr int NT = 256;              // threads per CTA
-constexpr int TM = 64, TN = 64;      // tile job shape
-constexpr int KC = 16;               // K chunk per pipeline stage
-constexpr int NSTAGE = 4;
+// Optional per-phase cycle counters (LuArgs::phase_cycles != nullptr): thread 0
+// accumulates clock64() deltas between CTA-wide barriers into 8 slots per leaf:
+// 0 U-part tiles, 1 L-part tiles, 2 panel strips+updates, 3 Linv, 4 trailing.
+#define PHASE_MARK(slot)                                                     \
+  do {                                                                       \
+    if (pc && threadIdx.x == 0) {                                            \
+      const long long now__ = clock64();                                     \
+      pc[slot] += now__ - t_phase;                                           \
+      t_phase = now__;                                                       \
+    }                                                                        \
+  } while (0)
+
+constexpr int NT = 256;              // threads per CTA (8 warps, 32x32 warp tiles)
+#ifndef HPS_KC
+#define HPS_KC 16
+#endif
+#ifndef HPS_NSTAGE
+#define HPS_NSTAGE 3
+#endif
+constexpr int KC = HPS_KC;           // K chunk per pipeline stage
+constexpr int NSTAGE = HPS_NSTAGE;
 constexpr int LDA_S = KC + 4;        // 20 doubles: conflict-free A fragment loads
-constexpr int LDB_S = TN + 4;        // 68 doubles: conflict-free B fragment loads
-constexpr int STAGE_DBL = TM * LDA_S + KC * LDB_S;   // 2368 doubles
-constexpr int PIPE_DBL = NSTAGE * STAGE_DBL;         // 9472 doubles = 75.8 KB
 constexpr int NSLOT = 8;             // strip rows per thread: R <= 2048 (p <= 45)
-constexpr int MAX_RPAD = 2048;
+constexpr int MAX_RPAD = 2048 + 128; // perm entries (tile gathers may run 127 past R)
+
+// Tile jobs C(TM x TN) <- C -/+ A(TM x K) B(K x TN): 128x64 for the L part and the
+// D rows (row-tall), 64x128 for the U part (row-wide).  Stage: A TM x KC (+4 pad),
+// B KC x TN (+4 pad); both pads make the m8n8k4 fragment loads bank-conflict free.
+template <int TM_, int TN_>
+struct Tile {
+  static constexpr int WM = TM_ / 32, WN = TN_ / 32;   // warp grid, WM * WN == 8
+  static constexpr int LDB = TN_ + 4;
+  static constexpr int STAGE = TM_ * LDA_S + KC * LDB;
+  static constexpr int AGR = TM_ * KC / 2 / NT;       // 16-byte A granules / thread / chunk
+  static constexpr int BGR = KC * TN_ / 2 / NT;       // 16-byte B granules / thread / chunk
+  static constexpr int BROW = TN_ / 2;                // granules per B row
+  static_assert(WM * WN == NT / 32, "8 warps");
+};
+using TileL = Tile<128, 64>;
+using TileU = Tile<64, 128>;
+constexpr int LS_U = 132;            // Linv-apply staging of a 64x128 U tile (== 4 mod 16)
+constexpr int cmax(int a, int b) { return a > b ? a : b; }
+constexpr int PIPE_DBL = cmax(cmax(NSTAGE * TileL::STAGE, NSTAGE * TileU::STAGE), 64 * LS_U);
 
 struct Smem {
   double pipe[PIPE_DBL];             // tile-job pipeline, re-used by the panel code
-  double piv[4];                     // current pivot row (strip)
-  double redv[NT / 32];
-  int redl[NT / 32];
-  int redp[NT / 32];
-  short perm[MAX_RPAD];
+  unsigned long long full[NSTAGE];   // stage filled (256 thread arrivals)
+  unsigned long long empty[NSTAGE];  // stage consumed (8 warp arrivals)
+  unsigned gchunk;                   // running K-chunk counter of this CTA
+  double wrow[2][NT / 32][4];        // per-warp pivot candidate rows (double-buffered)
+  unsigned long long redk[2][NT / 32];
+  short perm[MAX_RPAD];              // logical -> physical row
+  short iperm[MAX_RPAD];             // physical -> logical row
 };
 
-// ---------------------------------------------------------------------------
-// Tile job: acc = Cinit - A * B  (or + when sign = +1)
-// ---------------------------------------------------------------------------
+// Accumulator of one 32x32 warp tile: 4x4 DMMA 8x8 tiles, 2 doubles per lane each.
 struct Acc {
-  double v[2][4][2];
+  double v[4][4][2];
 };
 
-template <class ARow, class BRow>
-__device__ __forceinline__ void load_chunk(double* st, const ARow& arow, const BRow& brow, int k0,
-                                           int K) {
+template <class TL>
+__device__ __forceinline__ int acc_row(int mi) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  return 32 * (warp % TL::WM) + 8 * mi + (lane >> 2);
+}
+template <class TL>
+__device__ __forceinline__ int acc_col(int ni) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  return 32 * (warp / TL::WM) + 8 * ni + 2 * (lane & 3);
+}
+
+// Stage one K chunk.  Full chunks: per-thread A row pointers fixed for the whole tile
+// job, B rows re-gathered through perm each chunk.  K tail: predicated element loads
+// with zero fill (k >= K contributes nothing).
+// Stage one K chunk.  Full chunks: per-thread A row pointers fixed for the whole tile
+// job, B rows re-gathered through perm each chunk, cp.async with an mbarrier arrival on
+// completion.  K tail: predicated element loads with zero fill (k >= K contributes
+// nothing) followed by a plain arrival.
+template <class TL, class ARow, class BRow>
+__device__ __forceinline__ void load_chunk(double* st, unsigned long long* full, const double* const* pa,
+                                           const ARow& arow, const BRow& brow, int k0, int K) {
   double* As = st;
-  double* Bs = st + TM * LDA_S;
+  double* Bs = st + (TL::WM * 32) * LDA_S;
   const int tid = threadIdx.x;
+  constexpr int TM_ = TL::WM * 32, TN_ = TL::WN * 32;
   if (k0 + KC <= K) {
 #pragma unroll
-    for (int rep = 0; rep < 2; ++rep) {
-      const int g = tid + rep * NT;
-      const int row = g >> 3, seg = g & 7;
-      cp_async16(As + row * LDA_S + 2 * seg, arow(row) + k0 + 2 * seg);
+    for (int r = 0; r < TL::AGR; ++r) {
+      const int gi = tid + r * NT;
+      cp_async16(As + (gi / (KC / 2)) * LDA_S + 2 * (gi % (KC / 2)), pa[r] + k0);
     }
 #pragma unroll
-    for (int rep = 0; rep < 2; ++rep) {
-      const int g = tid + rep * NT;
-      const int row = g >> 5, seg = g & 31;
-      cp_async16(Bs + row * LDB_S + 2 * seg, brow(k0 + row) + 2 * seg);
+    for (int r = 0; r < TL::BGR; ++r) {
+      const int gi = tid + r * NT;
+      const int row = gi / TL::BROW, seg = gi % TL::BROW;
+      cp_async16(Bs + row * TL::LDB + 2 * seg, brow(k0 + row) + 2 * seg);
     }
-  } else {  // K tail: predicated element loads, zero fill (k >= K contributes nothing)
-    for (int e = tid; e < TM * KC; e += NT) {
+    cp_async_mbar_arrive(full);
+  } else {
+    for (int e = tid; e < TM_ * KC; e += NT) {
       const int row = e / KC, col = e % KC;
       As[row * LDA_S + col] = (k0 + col < K) ? arow(row)[k0 + col] : 0.0;
     }
-    for (int e = tid; e < KC * TN; e += NT) {
-      const int row = e / TN, col = e % TN;
-      Bs[row * LDB_S + col] = (k0 + row < K) ? brow(k0 + row)[col] : 0.0;
+    for (int e = tid; e < KC * TN_; e += NT) {
+      const int row = e / TN_, col = e % TN_;
+      Bs[row * TL::LDB + col] = (k0 + row < K) ? brow(k0 + row)[col] : 0.0;
     }
+    mbar_arrive(full);
   }
 }
 
-template <class ARow, class BRow>
-__device__ void tile_mma(Acc& acc, const ARow& arow, const BRow& brow, int K, double sign,
-                         double* pipe) {
+// Tile job mainloop: NSTAGE-deep cp.async pipeline synchronised by per-stage mbarriers
+// (full: 256 thread arrivals as copies land; empty: 8 warp arrivals as a stage is
+// consumed) instead of a CTA-wide barrier per K chunk.  Chunks are numbered per CTA
+// (sm->gchunk) across tile jobs so the barrier phases stay consistent.
+template <class TL, class ARow, class BRow, class Init>
+__device__ void tile_mma(Acc& acc, const Init& init, const ARow& arow, const BRow& brow, int K,
+                         double sign, double* pipe, unsigned long long* full,
+                         unsigned long long* empty, unsigned* gchunk) {
   const int nch = (K + KC - 1) / KC;
-  if (nch == 0) return;
+  if (nch == 0) {
+    init(acc);
+    return;
+  }
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = warp & 3, wn = warp >> 2;
+  const int wm = warp % TL::WM, wn = warp / TL::WM;
+  const unsigned g0 = *gchunk;
+  const double* pa[TL::AGR];
 #pragma unroll
-  for (int s = 0; s < NSTAGE - 1; ++s) {
-    if (s < nch) load_chunk(pipe + s * STAGE_DBL, arow, brow, s * KC, K);
-    cp_async_commit();
+  for (int r = 0; r < TL::AGR; ++r) {
+    const int gi = threadIdx.x + r * NT;
+    pa[r] = arow(gi / (KC / 2)) + 2 * (gi % (KC / 2));
   }
+  auto fill = [&](int c) {
+    const unsigned gf = g0 + c;
+    const int st = gf % NSTAGE;
+    if (gf >= NSTAGE) mbar_wait(&empty[st], ((gf - NSTAGE) / NSTAGE) & 1u);
+    load_chunk<TL>(pipe + st * TL::STAGE, &full[st], pa, arow, brow, c * KC, K);
+  };
+#pragma unroll
+  for (int s = 0; s < NSTAGE - 1; ++s)
+    if (s < nch) fill(s);
+  init(acc);   // C-init (load or first-touch assembly) overlaps the prologue copies
   for (int c = 0; c < nch; ++c) {
-    cp_async_wait<NSTAGE - 2>();
-    __syncthreads();
-    {
-      const int cn = c + NSTAGE - 1;
-      if (cn < nch) load_chunk(pipe + (cn % NSTAGE) * STAGE_DBL, arow, brow, cn * KC, K);
-      cp_async_commit();
-    }
-    const double* As = pipe + (c % NSTAGE) * STAGE_DBL;
-    const double* Bs = As + TM * LDA_S;
+    if (c + NSTAGE - 1 < nch) fill(c + NSTAGE - 1);
+    const unsigned gc = g0 + c;
+    const int st = gc % NSTAGE;
+    mbar_wait(&full[st], (gc / NSTAGE) & 1u);
+    const double* As = pipe + st * TL::STAGE;
+    const double* Bs = As + (TL::WM * 32) * LDA_S;
 #pragma unroll
     for (int kk = 0; kk < KC / 4; ++kk) {
-      double a[2], b[4];
+      double a[4], b[4];
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi) a[mi] = sign * As[(16 * wm + 8 * mi + g) * LDA_S + 4 * kk + t];
+      for (int mi = 0; mi < 4; ++mi) a[mi] = sign * As[(32 * wm + 8 * mi + g) * LDA_S + 4 * kk + t];
 #pragma unroll
-      for (int ni = 0; ni < 4; ++ni) b[ni] = Bs[(4 * kk + t) * LDB_S + 32 * wn + 8 * ni + g];
+      for (int ni = 0; ni < 4; ++ni) b[ni] = Bs[(4 * kk + t) * TL::LDB + 32 * wn + 8 * ni + g];
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi)
+      for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni) dmma(acc.v[mi][ni][0], acc.v[mi][ni][1], a[mi], b[ni]);
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
   }
-  cp_async_wait<0>();
+  __syncthreads();
+  if (threadIdx.x == 0) *gchunk = g0 + nch;
   __syncthreads();
 }
 
-// Fragment element (mi, ni, h) <-> tile row/col.
-__device__ __forceinline__ int acc_row(int mi) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  return 16 * (warp & 3) + 8 * mi + (lane >> 2);
-}
-__device__ __forceinline__ int acc_col(int ni) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  return 32 * (warp >> 2) + 8 * ni + 2 * (lane & 3);
-}
-
-template <class CRow>
+// C tile element access, rows masked by nrows, columns by ncols.
+template <class TL, class CRow>
 __device__ __forceinline__ void acc_load(Acc& acc, const CRow& crow, int nrows) {
 #pragma unroll
-  for (int mi = 0; mi < 2; ++mi) {
-    const int r = acc_row(mi);
+  for (int mi = 0; mi < 4; ++mi) {
+    const int r = acc_row<TL>(mi);
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) {
       if (r < nrows) {
-        const double2 v = *reinterpret_cast<const double2*>(crow(r) + acc_col(ni));
+        const double2 v = *reinterpret_cast<const double2*>(crow(r) + acc_col<TL>(ni));
         acc.v[mi][ni][0] = v.x;
         acc.v[mi][ni][1] = v.y;
       } else {
@@ -158,24 +223,94 @@ __device__ __forceinline__ void acc_load(Acc& acc, const CRow& crow, int nrows) 
   }
 }
 
+// Original operator entries of a tile (fused first-touch assembly): logical rows
+// base+r gathered through perm, columns c0 + tile column.
+struct Orig {
+  const int* rowcode;
+  const int* colcode;
+  const double* Ds;
+  const double* D2;
+  double k2;
+  const double* bl;
+  const double* fl;
+  int p;
+  bool inj;
+};
+
+template <class TL>
+__device__ __forceinline__ void acc_init_orig(Acc& acc, const Orig& o, const LeafDims& d,
+                                              const short* perm, int base, int c0, int nrows) {
+  int cc[8];
+#pragma unroll
+  for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) cc[2 * ni + h] = col_code_of(c0 + acc_col<TL>(ni) + h, d.p, d.ni, d.tb0, d.nb);
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int r = acc_row<TL>(mi);
+    const int phys = perm[base + r];
+    const int rc = r < nrows ? row_code_of(phys, d.p, d.ni, d.R) : (3 << 16);
+    const bool zrow = o.inj && phys == 0;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        acc.v[mi][ni][h] = aug_value(rc, cc[2 * ni + h], o.p, o.Ds, o.D2, o.k2, o.bl, o.fl, zrow);
+  }
+}
+
 __device__ __forceinline__ void acc_zero(Acc& acc) {
 #pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
+  for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) acc.v[mi][ni][0] = acc.v[mi][ni][1] = 0.0;
 }
 
-template <class CRow>
-__device__ __forceinline__ void acc_store(const Acc& acc, const CRow& crow, int nrows) {
+template <class TL, class CRow>
+__device__ __forceinline__ void acc_store(const Acc& acc, const CRow& crow, int nrows, int ncols) {
 #pragma unroll
-  for (int mi = 0; mi < 2; ++mi) {
-    const int r = acc_row(mi);
+  for (int mi = 0; mi < 4; ++mi) {
+    const int r = acc_row<TL>(mi);
     if (r >= nrows) continue;
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni)
-      *reinterpret_cast<double2*>(crow(r) + acc_col(ni)) =
-          make_double2(acc.v[mi][ni][0], acc.v[mi][ni][1]);
+    for (int ni = 0; ni < 4; ++ni) {
+      const int c = acc_col<TL>(ni);
+      if (c + 1 < ncols)
+        *reinterpret_cast<double2*>(crow(r) + c) = make_double2(acc.v[mi][ni][0], acc.v[mi][ni][1]);
+      else if (c < ncols)
+        crow(r)[c] = acc.v[mi][ni][0];
+    }
   }
+}
+
+// U-part epilogue: acc (64x128 tile) <- Linv (64x64) * acc.  The tile goes through
+// shared memory; Linv fragments come straight from global (32 KB per block row, L1/L2
+// resident across the block row's tiles).
+__device__ __forceinline__ void linv_apply(Acc& acc, const double* __restrict__ linv, double* pipe) {
+  double* Cs = pipe;   // 64 x LS_U
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni)
+      *reinterpret_cast<double2*>(Cs + acc_row<TileU>(mi) * LS_U + acc_col<TileU>(ni)) =
+          make_double2(acc.v[mi][ni][0], acc.v[mi][ni][1]);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int wm = warp % TileU::WM, wn = warp / TileU::WM;
+  acc_zero(acc);
+#pragma unroll 4
+  for (int kk = 0; kk < 16; ++kk) {
+    double av[4], bv[4];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) av[mi] = __ldg(linv + (32 * wm + 8 * mi + g) * 64 + 4 * kk + t);
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) bv[ni] = Cs[(4 * kk + t) * LS_U + 32 * wn + 8 * ni + g];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) dmma(acc.v[mi][ni][0], acc.v[mi][ni][1], av[mi], bv[ni]);
+  }
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------------------
@@ -192,181 +327,269 @@ __device__ __forceinline__ double* mrow(const LeafCtx& L, int logical) {
   return L.M + (size_t)L.perm[logical] * L.ld;
 }
 
-// Factor columns [e, e+sw) (sw <= 4) over logical rows [e, R): pivot search among
-// not-yet-pivoted A_ii rows, register-resident rows, 2 barriers per column.
+// Factor columns [e, e+sw) (sw <= 4) over logical rows [e, R) with register-resident
+// rows and ONE barrier per column.  Pivot search: every candidate (not yet pivoted A_ii
+// row, physical id < ni <= 2047) becomes a 64-bit key  bits(|v|) with its low 11 mantissa
+// bits replaced by (2047 - phys)  -- an order-preserving, symmetric arg-max that costs one
+// integer max per comparison; magnitudes closer than 2^-41 relative are treated as ties
+// and resolved by the smaller physical row (deterministic for any thread mapping).  Each
+// warp publishes its winner and that row's strip values (double-buffered slots), so the
+// pivot row needs no second broadcast round.  Interchanges are bookkeeping only: thread 0
+// swaps perm/iperm after the barrier; nobody else reads them inside the strip.
+__device__ __forceinline__ unsigned long long pivot_key(double v, int phys) {
+  return (static_cast<unsigned long long>(__double_as_longlong(fabs(v))) & ~0x7FFull) |
+         static_cast<unsigned long long>(0x7FF - phys);
+}
+
 __device__ void base_strip(const LeafCtx& L, int e, int sw, double& minpiv) {
   Smem* sm = L.sm;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nrows = L.R - e;
   double x[NSLOT][4];
-  int phys[NSLOT], lpos[NSLOT];
+  int phys[NSLOT];
+  unsigned active = 0;   // bit s: slot holds a row that is not yet pivoted
 #pragma unroll
   for (int s = 0; s < NSLOT; ++s) {
     const int idx = tid + s * NT;
-    phys[s] = -1;
-    lpos[s] = INT_MAX;
+    phys[s] = 0x7FFF;
     x[s][0] = x[s][1] = x[s][2] = x[s][3] = 0.0;
     if (idx < nrows) {
-      lpos[s] = e + idx;
       phys[s] = L.perm[e + idx];
+      active |= 1u << s;
       const double* src = L.M + (size_t)phys[s] * L.ld + e;
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         if (j < sw) x[s][j] = src[j];
     }
   }
-  __syncthreads();  // everyone has read perm[] before thread 0 starts swapping
+  __syncthreads();  // all perm reads done before thread 0 starts swapping
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     if (j >= sw) break;
     const int col = e + j;
-    const int p_old = L.perm[col];
-    double best = -1.0;
-    int bl = INT_MAX, bp = -1;
+    const int buf = j & 1;
+    unsigned long long best = 0ull;
+    int bs = 0;
 #pragma unroll
     for (int s = 0; s < NSLOT; ++s) {
-      if (phys[s] >= 0 && phys[s] < L.ni && lpos[s] >= col) {
-        const double v = fabs(x[s][j]);
-        if (v > best || (v == best && lpos[s] < bl)) { best = v; bl = lpos[s]; bp = phys[s]; }
-      }
+      const unsigned long long k =
+          ((active >> s) & 1u) && phys[s] < L.ni ? pivot_key(x[s][j], phys[s]) : 0ull;
+      if (k > best) { best = k; bs = s; }
     }
+    unsigned long long wbest = best;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-      const int ol = __shfl_xor_sync(0xffffffffu, bl, o);
-      const int op = __shfl_xor_sync(0xffffffffu, bp, o);
-      if (ov > best || (ov == best && ol < bl)) { best = ov; bl = ol; bp = op; }
+      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, wbest, o);
+      wbest = ok > wbest ? ok : wbest;
     }
-    if (lane == 0) { sm->redv[warp] = best; sm->redl[warp] = bl; sm->redp[warp] = bp; }
+    if (lane == 0) sm->redk[buf][warp] = wbest;
+    if (best == wbest && best != 0ull) {  // this lane owns the warp's candidate row
+      double r0 = x[0][0], r1 = x[0][1], r2 = x[0][2], r3 = x[0][3];
+#pragma unroll
+      for (int s = 1; s < NSLOT; ++s)
+        if (s == bs) { r0 = x[s][0]; r1 = x[s][1]; r2 = x[s][2]; r3 = x[s][3]; }
+      sm->wrow[buf][warp][0] = r0;
+      sm->wrow[buf][warp][1] = r1;
+      sm->wrow[buf][warp][2] = r2;
+      sm->wrow[buf][warp][3] = r3;
+    }
     __syncthreads();
-    best = sm->redv[0]; bl = sm->redl[0]; bp = sm->redp[0];
+    unsigned long long kb = sm->redk[buf][0];
+    int ww = 0;
 #pragma unroll
     for (int w = 1; w < NT / 32; ++w) {
-      const double ov = sm->redv[w];
-      const int ol = sm->redl[w];
-      if (ov > best || (ov == best && ol < bl)) { best = ov; bl = ol; bp = sm->redp[w]; }
+      const unsigned long long k = sm->redk[buf][w];
+      if (k > kb) { kb = k; ww = w; }
     }
-    // pivot row owner publishes its (already updated) strip row
+    const int pphys = 0x7FF - static_cast<int>(kb & 0x7FFull);
+    double prow[4];
 #pragma unroll
-    for (int s = 0; s < NSLOT; ++s)
-      if (phys[s] == bp) {
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj) sm->piv[jj] = x[s][jj];
-      }
+    for (int jj = 0; jj < 4; ++jj) prow[jj] = sm->wrow[buf][ww][jj];
+    const double piv = prow[j];
+    const double rpiv = 1.0 / piv;   // dgetf2-style reciprocal scaling
     if (tid == 0) {
-      L.perm[col] = (short)bp;
-      L.perm[bl] = (short)p_old;
+      minpiv = fmin(minpiv, fabs(piv));
+      const int q = sm->iperm[pphys];
+      const int pold = L.perm[col];
+      L.perm[col] = (short)pphys;
+      L.perm[q] = (short)pold;
+      sm->iperm[pphys] = (short)col;
+      sm->iperm[pold] = (short)q;
     }
-    __syncthreads();
-    const double piv = sm->piv[j];
-    if (tid == 0) minpiv = fmin(minpiv, fabs(piv));
 #pragma unroll
     for (int s = 0; s < NSLOT; ++s) {
-      if (phys[s] == bp) lpos[s] = col;
-      else if (phys[s] == p_old) lpos[s] = bl;
-      if (phys[s] >= 0 && lpos[s] > col) {
-        const double l = x[s][j] / piv;
+      if (phys[s] == pphys) active &= ~(1u << s);
+      if ((active >> s) & 1u) {
+        const double l = x[s][j] * rpiv;
         x[s][j] = l;
 #pragma unroll
         for (int jj = 0; jj < 4; ++jj)
-          if (jj > j && jj < sw) x[s][jj] = fma(-l, sm->piv[jj], x[s][jj]);
+          if (jj > j && jj < sw) x[s][jj] = fma(-l, prow[jj], x[s][jj]);
       }
     }
   }
 #pragma unroll
   for (int s = 0; s < NSLOT; ++s) {
-    if (phys[s] < 0) continue;
+    if (phys[s] == 0x7FFF) continue;
     double* dst = L.M + (size_t)phys[s] * L.ld + e;
 #pragma unroll
     for (int j = 0; j < 4; ++j)
       if (j < sw) dst[j] = x[s][j];
   }
+  __threadfence_block();
   __syncthreads();
+}
+
+constexpr int XS = 36;  // stride of the in-panel h x nd blocks (== 4 mod 16: conflict-free B fragments)
+
+// Recursive-LU update inside a panel: source columns [s0, s0+h) are factored,
+// destination columns [d0, d0+nd) (d0 = s0+h) carry all earlier updates.
+//   U part (rows s0..s0+h-1):  X = L_hh^{-1} X     one warp, column per lane, no barriers
+//   L part (rows d0..R-1)   :  C -= A[:, src] X    DMMA m8n8k4, one 8-row group per warp
+template <int H>
+__device__ void panel_update_t(const LeafCtx& L, int s0, int d0, int nd, long long* pc,
+                               long long& t_phase) {
+  constexpr int NTILE = (H + 7) / 8;        // 8-wide DMMA column tiles (nd <= H)
+  constexpr int UNR = H <= 8 ? 4 : 2;       // 8-row groups in flight per warp
+  constexpr int KS = H / 4;                 // DMMA k-steps
+  Smem* sm = L.sm;
+  double* Ls = sm->pipe;               // H x H   (stride XS)
+  double* X = sm->pipe + 32 * XS;      // H x 8*NTILE (stride XS), zero padded
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < H * H; e += NT) {
+    const int i = e / H, k = e % H;
+    Ls[i * XS + k] = (k < i) ? mrow(L, s0 + i)[s0 + k] : 0.0;
+  }
+  for (int e = tid; e < H * 8 * NTILE; e += NT) {
+    const int i = e / (8 * NTILE), j = e % (8 * NTILE);
+    X[i * XS + j] = j < nd ? mrow(L, s0 + i)[d0 + j] : 0.0;
+  }
+  __syncthreads();
+  if (warp == 0 && lane < nd) {  // U part: one column per lane, registers, no barriers
+    double x[H];
+#pragma unroll
+    for (int i = 0; i < H; ++i) x[i] = X[i * XS + lane];
+#pragma unroll
+    for (int k = 0; k < H - 1; ++k)
+#pragma unroll
+      for (int i = k + 1; i < H; ++i) x[i] = fma(-Ls[i * XS + k], x[k], x[i]);
+#pragma unroll
+    for (int i = 0; i < H; ++i) X[i * XS + lane] = x[i];
+  }
+  __syncthreads();
+  for (int e = tid; e < H * nd; e += NT) {
+    const int i = e / nd, j = e % nd;
+    mrow(L, s0 + i)[d0 + j] = X[i * XS + j];
+  }
+  PHASE_MARK(6);
+  // L part with DMMA: rows logical [d0, R) in 8-row groups; each warp keeps UNR groups'
+  // loads in flight before computing.
+  const int g = lane >> 2, t = lane & 3;
+  for (int base = d0 + 8 * warp; base < L.R; base += 8 * (NT / 32) * UNR) {
+    double acc[UNR][NTILE][2];
+    double a[UNR][KS];
+    double* row[UNR];
+    bool ok[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int r0 = base + 8 * (NT / 32) * u;
+      const int r = r0 + g;
+      ok[u] = r < L.R;
+      row[u] = L.M + (size_t)L.perm[ok[u] ? r : min(r0, L.R - 1)] * L.ld;
+#pragma unroll
+      for (int ni = 0; ni < NTILE; ++ni) {
+        const double2 c = *reinterpret_cast<const double2*>(row[u] + d0 + 8 * ni + 2 * t);
+        acc[u][ni][0] = c.x;
+        acc[u][ni][1] = c.y;
+      }
+#pragma unroll
+      for (int kk = 0; kk < KS; ++kk) a[u][kk] = -row[u][s0 + 4 * kk + t];
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u)
+#pragma unroll
+      for (int kk = 0; kk < KS; ++kk)
+#pragma unroll
+        for (int ni = 0; ni < NTILE; ++ni)
+          dmma(acc[u][ni][0], acc[u][ni][1], a[u][kk], X[(4 * kk + t) * XS + 8 * ni + g]);
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      if (!ok[u]) continue;
+#pragma unroll
+      for (int ni = 0; ni < NTILE; ++ni) {
+        const int c = 8 * ni + 2 * t;
+        if (c + 1 < nd) {
+          *reinterpret_cast<double2*>(row[u] + d0 + c) = make_double2(acc[u][ni][0], acc[u][ni][1]);
+        } else if (c < nd) {
+          row[u][d0 + c] = acc[u][ni][0];
+        }
+      }
+    }
+  }
+  __threadfence_block();
+  __syncthreads();
+  PHASE_MARK(7);
 }
 
 // Recursive-LU update inside a panel: source columns [s0, s0+h) are factored,
-// destination columns [d0, d0+nd) (d0 = s0+h) have all earlier updates.
-//   U part (rows s0..s0+h-1):  X = L_hh^{-1} X         (forward substitution)
-//   L part (rows d0..R-1)   :  C -= A[:, src] * X       (skinny FMA update)
-__device__ void panel_update(const LeafCtx& L, int s0, int h, int d0, int nd) {
-  Smem* sm = L.sm;
-  double* Ls = sm->pipe;              // h x h   (stride 33)
-  double* X = sm->pipe + 33 * 32;     // h x nd  (stride 33)
-  const int tid = threadIdx.x;
-  for (int e = tid; e < h * h; e += NT) {
-    const int i = e / h, k = e % h;
-    Ls[i * 33 + k] = (k < i) ? mrow(L, s0 + i)[s0 + k] : 0.0;
+// destination columns [d0, d0+nd) (d0 = s0+h) carry all earlier updates.
+//   U part (rows s0..s0+h-1):  X = L_hh^{-1} X     one warp, column per lane, registers
+//   L part (rows d0..R-1)   :  C -= A[:, src] X    DMMA m8n8k4 over 8-row groups
+__device__ void panel_update(const LeafCtx& L, int s0, int h, int d0, int nd, long long* pc,
+                             long long& t_phase) {
+  switch (h) {
+    case 4: panel_update_t<4>(L, s0, d0, nd, pc, t_phase); break;
+    case 8: panel_update_t<8>(L, s0, d0, nd, pc, t_phase); break;
+    case 16: panel_update_t<16>(L, s0, d0, nd, pc, t_phase); break;
+    default: panel_update_t<32>(L, s0, d0, nd, pc, t_phase); break;
   }
-  for (int e = tid; e < h * nd; e += NT) {
-    const int i = e / nd, j = e % nd;
-    X[i * 33 + j] = mrow(L, s0 + i)[d0 + j];
-  }
-  __syncthreads();
-  for (int k = 0; k < h - 1; ++k) {
-    for (int e = tid; e < (h - 1 - k) * nd; e += NT) {
-      const int i = k + 1 + e / nd, j = e % nd;
-      X[i * 33 + j] = fma(-Ls[i * 33 + k], X[k * 33 + j], X[i * 33 + j]);
-    }
-    __syncthreads();
-  }
-  for (int e = tid; e < h * nd; e += NT) {
-    const int i = e / nd, j = e % nd;
-    mrow(L, s0 + i)[d0 + j] = X[i * 33 + j];
-  }
-  // L part: rows logical [d0, R)
-  for (int r = d0 + tid; r < L.R; r += NT) {
-    double* row = mrow(L, r);
-    for (int j0 = 0; j0 < nd; j0 += 8) {
-      double acc[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) acc[j] = (j0 + j < nd) ? row[d0 + j0 + j] : 0.0;
-      for (int k = 0; k < h; ++k) {
-        const double a = row[s0 + k];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) acc[j] = fma(-a, X[k * 33 + j0 + j], acc[j]);
-      }
-#pragma unroll
-      for (int j = 0; j < 8; ++j)
-        if (j0 + j < nd) row[d0 + j0 + j] = acc[j];
-    }
-  }
-  __syncthreads();
 }
 
 // Inverse of the unit-lower diagonal block of panel [c0, c0+w) -> Linv (64x64,
-// identity-padded, row-major).
+// identity-padded, row-major).  Warp w owns columns 8w..8w+7; the four lanes of a
+// column hold 16 rows each in registers and step through k with a shuffle
+// broadcast of X[k][j] -- no block barriers inside.
 __device__ void panel_linv(const LeafCtx& L, int c0, int w, double* linv) {
   double* Ls = L.sm->pipe;            // 64 x 65
-  double* X = L.sm->pipe + 64 * 65;   // 64 x 65
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   for (int e = tid; e < 64 * 64; e += NT) {
     const int i = e >> 6, k = e & 63;
     Ls[i * 65 + k] = (i < w && k < i) ? mrow(L, c0 + i)[c0 + k] : 0.0;
-    X[i * 65 + k] = (i == k) ? 1.0 : 0.0;
   }
   __syncthreads();
-  // X <- L^{-1}: for k, rows i > k: X[i, :k+1] -= L[i,k] * X[k, :k+1]
-  for (int k = 0; k < w - 1; ++k) {
-    const int nr = w - 1 - k, ncol = k + 1;
-    for (int e = tid; e < nr * ncol; e += NT) {
-      const int i = k + 1 + e / ncol, j = e % ncol;
-      X[i * 65 + j] = fma(-Ls[i * 65 + k], X[k * 65 + j], X[i * 65 + j]);
+  const int j = 8 * warp + (lane >> 2), q = lane & 3;
+  double x[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) x[r] = (16 * q + r == j) ? 1.0 : 0.0;
+#pragma unroll
+  for (int qo = 0; qo < 4; ++qo) {
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      const int k = 16 * qo + kk;
+      const double xk = __shfl_sync(0xffffffffu, x[kk], (lane & ~3) | qo);
+      if (q >= qo) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+          if (16 * q + r > k) x[r] = fma(-Ls[(16 * q + r) * 65 + k], xk, x[r]);
+      }
     }
-    __syncthreads();
   }
-  for (int e = tid; e < 64 * 64; e += NT) linv[e] = X[(e >> 6) * 65 + (e & 63)];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) linv[(16 * q + r) * 64 + j] = x[r];
   __syncthreads();
 }
 
-__device__ void panel_factor(const LeafCtx& L, int c0, int w, double& minpiv) {
+__device__ void panel_factor(const LeafCtx& L, int c0, int w, double& minpiv, long long* pc,
+                             long long& t_phase) {
   for (int e = c0; e < c0 + w;) {
     const int sw = min(4, c0 + w - e);
     base_strip(L, e, sw, minpiv);
+    PHASE_MARK(5);
     e += sw;
     const int done = e - c0;
     if (done < w) {
       const int h = done & (-done);      // lowest set bit: recursive-LU schedule
-      panel_update(L, e - h, h, e, min(h, c0 + w - e));
+      panel_update(L, e - h, h, e, min(h, c0 + w - e), pc, t_phase);
     }
   }
 }
@@ -374,11 +597,8 @@ __device__ void panel_factor(const LeafCtx& L, int c0, int w, double& minpiv) {
 // ---------------------------------------------------------------------------
 // Kernel
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(NT, 2) k2_lu_schur_kernel(LuArgs a) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  Smem* sm = reinterpret_cast<Smem*>(smem_raw);
+__device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
   const LeafDims d = a.d;
-  const int leaf = blockIdx.x;
   LeafCtx L;
   L.M = a.ws + (size_t)leaf * d.leaf_stride;
   L.ld = d.ld;
@@ -390,10 +610,24 @@ __global__ void __launch_bounds__(NT, 2) k2_lu_schur_kernel(LuArgs a) {
   short* perm_g = a.perm + (size_t)leaf * d.Rpad;
   // Entries past Rpad are read by masked-out tile rows (e.g. the D-row tiles start at ni, which
   // need not be 64-aligned): point them at a valid row so the gathers stay in bounds.
-  for (int i = threadIdx.x; i < MAX_RPAD; i += NT)
+  for (int i = threadIdx.x; i < MAX_RPAD; i += NT) {
     sm->perm[i] = i < d.Rpad ? (a.factor ? (short)i : perm_g[i]) : (short)(d.Rpad - 1);
+    sm->iperm[i] = (short)i;   // only used while factoring (perm starts as the identity)
+  }
   __syncthreads();
   double minpiv = INFINITY;  // meaningful on thread 0
+  long long* pc = a.phase_cycles ? a.phase_cycles + (size_t)leaf * 8 : nullptr;
+  Orig orig;
+  orig.rowcode = a.rowcode;
+  orig.colcode = a.colcode;
+  orig.Ds = a.Ds;
+  orig.D2 = a.D2;
+  orig.k2 = a.k2;
+  orig.bl = a.b ? a.b + (size_t)leaf * d.p * d.p : nullptr;
+  orig.fl = a.f ? a.f + (size_t)leaf * d.p * d.p : nullptr;
+  orig.p = d.p;
+  orig.inj = a.inject && a.inject[leaf];
+  long long t_phase = clock64();
 
   const double* M = L.M;
   const int ld = d.ld;
@@ -402,95 +636,85 @@ __global__ void __launch_bounds__(NT, 2) k2_lu_schur_kernel(LuArgs a) {
     return [=](int i) -> const double* { return M + (size_t)perm[base + i] * ld; };
   };
 
-  // ---------------- A_ii block columns ----------------
-  for (int J = 0; J < (a.factor ? d.nblk : 0); ++J) {
+  // Crout-ordered blocked LU over 64-wide blocks J of A_ii:
+  //   (b) L part of block column J   rows [c0, R)      -= L[:, 0:c0] U[0:c0, J]   (K = c0)
+  //   (c) panel J factorisation (pivoting) + Linv_J
+  //   (a) U part of block row J      cols right of J   = Linv_J (A - L[J, 0:c0] U[0:c0, :])
+  // The U-part tiles of one block row are independent (no sequential block-row chain), and
+  // the Linv_J product is fused into the tile epilogue (shared memory, no HBM round trip).
+  for (int J = 0; J < d.nblk; ++J) {
     const int c0 = 64 * J;
     const int w = min(64, d.ni - c0);
-    // (a) U part: logical rows [64 I, 64 I + 64), I < J
-    for (int I = 0; I < J; ++I) {
-      const int r0 = 64 * I;
-      auto crow = [=](int i) -> double* { return L.M + (size_t)perm[r0 + i] * ld + c0; };
-      Acc acc;
-      acc_load(acc, crow, TM);
-      auto arow = lrow(r0);
-      auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + c0; };
-      tile_mma(acc, arow, brow, r0, -1.0, sm->pipe);
-      acc_store(acc, crow, TM);
+    if (a.factor) {
+      for (int rt = c0; rt < d.R; rt += 128) {
+        const int nr = min(128, d.R - rt);
+        auto crow = [=](int i) -> double* { return L.M + (size_t)perm[rt + i] * ld + c0; };
+        Acc acc;
+        auto init = [&](Acc& x) {
+          if (a.fused) acc_init_orig<TileL>(x, orig, d, perm, rt, c0, nr);
+          else acc_load<TileL>(x, crow, nr);
+        };
+        auto arow = lrow(rt);
+        auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + c0; };
+        tile_mma<TileL>(acc, init, arow, brow, c0, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
+        acc_store<TileL>(acc, crow, nr, 64);
+      }
       __threadfence_block();
       __syncthreads();
-      // X <- Linv_I * X
-      const double* li = Linv + (size_t)I * 4096;
-      acc_zero(acc);
-      auto arow2 = [=](int i) -> const double* { return li + i * 64; };
-      auto brow2 = [=](int k) -> const double* { return M + (size_t)perm[r0 + k] * ld + c0; };
-      tile_mma(acc, arow2, brow2, 64, 1.0, sm->pipe);
-      acc_store(acc, crow, TM);
-      __threadfence_block();
-      __syncthreads();
+      PHASE_MARK(1);
+      panel_factor(L, c0, w, minpiv, pc, t_phase);
+      PHASE_MARK(2);
+      panel_linv(L, c0, w, Linv + (size_t)J * 4096);
+      PHASE_MARK(3);
     }
-    // (b) L part: logical rows [c0, R)
-    for (int rt = c0; rt < d.R; rt += TM) {
-      const int nr = min(TM, d.R - rt);
-      auto crow = [=](int i) -> double* { return L.M + (size_t)perm[rt + i] * ld + c0; };
+    const double* li = Linv + (size_t)J * 4096;
+    const int ct_begin = a.factor ? c0 + 64 : d.tb0;
+    const int ct_end = d.tb0 + 64 * d.ntb;
+    for (int ct = ct_begin; ct < ct_end; ct += 128) {
+      auto crow = [=](int i) -> double* { return L.M + (size_t)perm[c0 + i] * ld + ct; };
       Acc acc;
-      acc_load(acc, crow, nr);
-      auto arow = lrow(rt);
-      auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + c0; };
-      tile_mma(acc, arow, brow, c0, -1.0, sm->pipe);
-      acc_store(acc, crow, nr);
+      auto init = [&](Acc& x) {
+        if (a.fused) acc_init_orig<TileU>(x, orig, d, perm, c0, ct, 64);
+        else acc_load<TileU>(x, crow, 64);
+      };
+      auto arow = lrow(c0);
+      auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + ct; };
+      tile_mma<TileU>(acc, init, arow, brow, c0, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
+      linv_apply(acc, li, sm->pipe);
+      acc_store<TileU>(acc, crow, w, min(128, ct_end - ct));
     }
     __threadfence_block();
     __syncthreads();
-    // (c) panel factorisation + inverse of its unit-lower diagonal block
-    panel_factor(L, c0, w, minpiv);
-    panel_linv(L, c0, w, Linv + (size_t)J * 4096);
+    PHASE_MARK(0);
   }
 
-  // ---------------- trailing columns [A_ib | f] ----------------
+  // ---------------- D rows of the trailing columns ----------------
+  // T = D_b - L21 U12 ; -w = 0 - L21 (L^{-1} f)      (K = ni)
   for (int tb = 0; tb < d.ntb; ++tb) {
     const int c0 = d.tb0 + 64 * tb;
-    for (int I = 0; I < d.nblk; ++I) {
-      const int r0 = 64 * I;
-      const int nr = min(TM, d.ni - r0);
-      auto crow = [=](int i) -> double* { return L.M + (size_t)perm[r0 + i] * ld + c0; };
-      Acc acc;
-      acc_load(acc, crow, TM);
-      auto arow = lrow(r0);
-      auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + c0; };
-      tile_mma(acc, arow, brow, r0, -1.0, sm->pipe);
-      acc_store(acc, crow, nr);
-      __threadfence_block();
-      __syncthreads();
-      const double* li = Linv + (size_t)I * 4096;
-      acc_zero(acc);
-      auto arow2 = [=](int i) -> const double* { return li + i * 64; };
-      auto brow2 = [=](int k) -> const double* { return M + (size_t)perm[r0 + k] * ld + c0; };
-      tile_mma(acc, arow2, brow2, 64, 1.0, sm->pipe);
-      acc_store(acc, crow, nr);
-      __threadfence_block();
-      __syncthreads();
-    }
-    // D rows: T = D_b - L21 U12 ; -w = 0 - L21 (L^{-1} f)
     double* Tl = a.T_out + (size_t)leaf * d.nb * d.nb;
     double* wl = a.w_out + (size_t)leaf * d.nb;
-    for (int rt = d.ni; rt < d.R; rt += TM) {
-      const int nr = min(TM, d.R - rt);
+    for (int rt = d.ni; rt < d.R; rt += 128) {
+      const int nr = min(128, d.R - rt);
       auto crow = [=](int i) -> double* { return L.M + (size_t)perm[rt + i] * ld + c0; };
       Acc acc;
-      acc_load(acc, crow, nr);
+      auto init = [&](Acc& x) {
+        if (a.fused) acc_init_orig<TileL>(x, orig, d, perm, rt, c0, nr);
+        else acc_load<TileL>(x, crow, nr);
+      };
       auto arow = lrow(rt);
       auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + c0; };
-      tile_mma(acc, arow, brow, d.ni, -1.0, sm->pipe);
+      tile_mma<TileL>(acc, init, arow, brow, d.ni, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
 #pragma unroll
-      for (int mi = 0; mi < 2; ++mi) {
-        const int r = acc_row(mi);
+      for (int mi = 0; mi < 4; ++mi) {
+        const int r = acc_row<TileL>(mi);
         if (r >= nr) continue;
         const int trow = rt + r - d.ni;
 #pragma unroll
         for (int ni2 = 0; ni2 < 4; ++ni2) {
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
-            const int tc = 64 * tb + acc_col(ni2) + hh;
+            const int tc = 64 * tb + acc_col<TileL>(ni2) + hh;
             if (tc < d.nb) Tl[(size_t)trow * d.nb + tc] = acc.v[mi][ni2][hh];
             else if (tc == d.nb) wl[trow] = -acc.v[mi][ni2][hh];
           }
@@ -498,7 +722,12 @@ __global__ void __launch_bounds__(NT, 2) k2_lu_schur_kernel(LuArgs a) {
       }
     }
   }
-  if (!a.factor) return;
+  __syncthreads();
+  PHASE_MARK(4);
+  if (!a.factor) {
+    __syncthreads();
+    return;
+  }
   __syncthreads();
   for (int i = threadIdx.x; i < d.Rpad; i += NT) perm_g[i] = sm->perm[i];
   if (threadIdx.x == 0) {
@@ -507,6 +736,29 @@ __global__ void __launch_bounds__(NT, 2) k2_lu_schur_kernel(LuArgs a) {
     if (a.minratio) a.minratio[leaf] = ratio;
     a.status[leaf] = (ratio >= 1e-12) ? 0 : 1;
   }
+  __syncthreads();
+}
+
+// Persistent: grid = 2 CTAs per SM, each walks leaves blockIdx.x, +gridDim.x, ...
+// The second CTA of every SM (blockIdx >= gridDim/2; classic placement puts b and
+// b + #SM on one SM) starts `dephase_ns` late so the two co-resident leaves are not in
+// their (latency-bound) panel phases at the same time.
+__global__ void __launch_bounds__(NT, 2) k2_lu_schur_kernel(LuArgs a, int n_leaves) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem* sm = reinterpret_cast<Smem*>(smem_raw);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(&sm->full[s], NT);
+      mbar_init(&sm->empty[s], NT / 32);
+    }
+    sm->gchunk = 0;
+  }
+  __syncthreads();
+  if (a.dephase_ns > 0 && blockIdx.x >= (gridDim.x + 1) / 2) {
+    const long long t0 = globaltimer();
+    while (globaltimer() - t0 < a.dephase_ns) __nanosleep(20000);
+  }
+  for (int leaf = blockIdx.x; leaf < n_leaves; leaf += gridDim.x) process_leaf(a, sm, leaf);
 }
 
 size_t lu_smem_bytes() { return sizeof(Smem); }
@@ -515,7 +767,11 @@ void launch_lu_schur(const LuArgs& a, int n_leaves, cudaStream_t st) {
   if (n_leaves <= 0) return;
   cudaFuncSetAttribute(k2_lu_schur_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(Smem));
-  k2_lu_schur_kernel<<<n_leaves, NT, sizeof(Smem), st>>>(a);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = n_leaves < 2 * sms ? n_leaves : 2 * sms;
+  k2_lu_schur_kernel<<<grid, NT, sizeof(Smem), st>>>(a, n_leaves);
 }
 
 }  // namespace hpsg

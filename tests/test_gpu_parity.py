@@ -243,3 +243,18 @@ def test_c4_subset_and_laplace_property():
     nc = [k for k in range(4 * (p - 1)) if k not in (0, p - 1, 2 * p - 2, 2 * p - 1)]
     flux = T @ np.ones(4 * (p - 1))
     assert np.max(np.abs(flux[:, nc])) <= 1e-9 * np.max(np.abs(T))
+
+
+def test_fused_assembly_equals_materialised_k1(monkeypatch):
+    """K2's first-touch assembly (HPS_FUSED=1) evaluates exactly K1's entries: T, w bitwise
+    equal to the K1-materialised default path."""
+    p, nx, ny, kappa = 16, 3, 3, 40.0
+    X, Y = P.leaf_coords(nx, ny, p)
+    b = P.crystal_field(X * 0.4 + 0.3, Y * 0.4 + 0.3); f = np.cos(5 * X) * Y
+    with G().LeafStage(p, nx, ny, kappa) as st:
+        T1, w1, _ = st.condense(b, f)
+    monkeypatch.setenv("HPS_FUSED", "1")
+    with G().LeafStage(p, nx, ny, kappa) as st:
+        T2, w2, _ = st.condense(b, f)
+    assert np.array_equal(T1.view(np.int64), T2.view(np.int64))
+    assert np.array_equal(w1.view(np.int64), w2.view(np.int64))

@@ -19,6 +19,23 @@ namespace hpsg {
 // grid (ceil(Rpad / kRows), n_leaves), block 256.
 constexpr int kRows = 8;
 
+// Boundary position of local node (y, x) on the leaf boundary (SPEC.md:314 order).
+__device__ __forceinline__ int boundary_pos(int y, int x, int p) {
+  if (y == 0) return x;                   // S (incl. SW, SE)
+  if (x == p - 1) return p - 1 + y;       // E (incl. NE)
+  if (y == p - 1) return 2 * p - 1 + x;   // N (incl. NW)
+  return 3 * p - 3 + y;                   // W
+}
+// Column of local node (y, x) in the augmented layout.
+__device__ __forceinline__ int node_col(int y, int x, int p, int tb0) {
+  if (y >= 1 && y <= p - 2 && x >= 1 && x <= p - 2) return (y - 1) * (p - 2) + (x - 1);
+  return tb0 + boundary_pos(y, x, p);
+}
+
+// K1: one CTA per kRows rows of one leaf.  Phase 1 streams zeros over the rows with
+// 16-byte stores (the operator is >95% zeros: HBM-write bound); phase 2 (after the
+// barrier) writes the <= 2(p-2)+5 structural nonzeros of each row -- one warp per row --
+// with exactly the entries a_entry / dn_entry evaluate (same IEEE sequence as the oracle).
 __global__ void __launch_bounds__(256) k1_assemble_kernel(
     LeafDims d, const int* __restrict__ rowcode, const int* __restrict__ colcode,
     const double* __restrict__ Ds, const double* __restrict__ D2, double k2,
@@ -26,22 +43,62 @@ __global__ void __launch_bounds__(256) k1_assemble_kernel(
     const int* __restrict__ inject) {
   const int leaf = blockIdx.y;
   const int r0 = blockIdx.x * kRows;
-  const int pp = d.p * d.p;
+  const int p = d.p, q = p - 2, pp = p * p;
   const double* bl = b + (size_t)leaf * pp;
   const double* fl = f + (size_t)leaf * pp;
   const bool inj = inject && inject[leaf];
   double* W = ws + (size_t)leaf * d.leaf_stride;
   const int half = d.ld >> 1;
-  for (int idx = threadIdx.x; idx < kRows * half; idx += blockDim.x) {
-    const int r = r0 + idx / half;
-    if (r >= d.Rpad) break;
-    const int c = (idx % half) * 2;
-    const int rc = __ldg(rowcode + r);
-    const bool zrow = inj && r == 0;
-    double2 v;
-    v.x = aug_value(rc, __ldg(colcode + c), d.p, Ds, D2, k2, bl, fl, zrow);
-    v.y = aug_value(rc, __ldg(colcode + c + 1), d.p, Ds, D2, k2, bl, fl, zrow);
-    reinterpret_cast<double2*>(W + (size_t)r * d.ld)[c >> 1] = v;
+  const int nrows = min(kRows, d.Rpad - r0);
+  double2* W2 = reinterpret_cast<double2*>(W + (size_t)r0 * d.ld);
+  for (int idx = threadIdx.x; idx < nrows * half; idx += blockDim.x) W2[idx] = make_double2(0.0, 0.0);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = r0 + warp;
+  if (warp >= nrows || r >= d.R) return;
+  double* row = W + (size_t)r * d.ld;
+  const int rc = __ldg(rowcode + r);
+  const int iy = rc & 255, ix = (rc >> 8) & 255;
+  if (r < d.ni) {
+    const int l = iy * p + ix;
+    // row line (jy == iy): interior columns jx = 1..q and the two boundary nodes (iy,0),(iy,p-1)
+    for (int jx = lane; jx < p; jx += 32) {
+      const bool interior = jx >= 1 && jx <= q;
+      if (interior && inj && r == 0) continue;
+      double v;
+      if (jx == ix) {
+        v = -__ldg(D2 + iy * p + iy);
+        v = __dsub_rn(v, __ldg(D2 + ix * p + ix));
+        v = __dsub_rn(v, __dmul_rn(k2, __ldg(bl + l)));
+      } else {
+        v = -__ldg(D2 + ix * p + jx);
+      }
+      row[node_col(iy, jx, p, d.tb0)] = v;
+    }
+    // column line (jx == ix, jy != iy): interior jy = 1..q and (0,ix), (p-1,ix)
+    for (int jy = lane; jy < p; jy += 32) {
+      if (jy == iy) continue;
+      const bool interior = jy >= 1 && jy <= q;
+      if (interior && inj && r == 0) continue;
+      row[node_col(jy, ix, p, d.tb0)] = -__ldg(D2 + iy * p + jy);
+    }
+    if (lane == 0) row[d.tb0 + d.nb] = __ldg(fl + l);
+  } else {
+    const int edge = (rc >> 18) & 3;
+    for (int j = lane; j < p; j += 32) {
+      int y, x;
+      double v;
+      if (edge == 0 || edge == 2) {   // S: -d/dy, N: +d/dy along the column line
+        y = j; x = ix;
+        v = __ldg(Ds + iy * p + j);
+        if (edge == 0) v = -v;
+      } else {                        // E: +d/dx, W: -d/dx along the row line
+        y = iy; x = j;
+        v = __ldg(Ds + ix * p + j);
+        if (edge == 3) v = -v;
+      }
+      row[node_col(y, x, p, d.tb0)] = v;
+    }
   }
 }
 

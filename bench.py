@@ -342,8 +342,9 @@ def main():
         traffic = None
         tpath = os.path.join(ROOT, "profiles", f"k2_traffic_p{p}.json")
         if os.path.exists(tpath):
-            try:
-                traffic = json.load(open(tpath)).get("bytes_per_launch")
+            try:   # ncu dram bytes per leaf x leaves of the average K2 launch (chunk)
+                chunks = max(1, -(-n // info["chunk_leaves"]))
+                traffic = json.load(open(tpath))["bytes_per_leaf"] * n / chunks
             except Exception:
                 traffic = None
         line = {
@@ -358,6 +359,7 @@ def main():
                          "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
                          "traffic": traffic, "peak_source": FP64_PEAK_NOTE,
                          "flops_per_leaf": f_leaf, "k2_ms_per_step_rank0": k2_ms,
+                         "traffic_unit": "DRAM bytes per K2 launch (ncu, scaled to the launch's leaves)",
                          "k1_ms_per_step_rank0": tim["ms_assemble"] / args.steps},
             "cpu_baseline": cpu,
             "e2e": e2e,

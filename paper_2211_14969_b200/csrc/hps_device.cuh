@@ -135,6 +135,17 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
 }
 
+// Long waits (cross-group hand-offs): try_wait with a suspend-time hint so idle warps
+// do not spin on the issue slots the working group needs.
+__device__ __forceinline__ void mbar_wait_sleep(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAITS_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      " @!p bra WAITS_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
+
 __device__ __forceinline__ long long globaltimer() {
   long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));

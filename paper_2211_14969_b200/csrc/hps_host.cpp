@@ -211,6 +211,9 @@ struct hps_gpu_ctx {
   // K1 materialises the operator (default); HPS_FUSED=1 evaluates the tile C-inits in K2
   // instead (first-touch assembly, no workspace writes by K1; slower in r01 measurements).
   bool fused = std::getenv("HPS_FUSED") != nullptr;
+  // Panel/GEMM lookahead kernel for condense (HPS_LOOKAHEAD=1); the default 2-leaves-per-SM
+  // kernel measured faster on C2/C3/C4 in round 1.
+  bool lookahead = std::getenv("HPS_LOOKAHEAD") && std::getenv("HPS_LOOKAHEAD")[0] == '1';
   long long dephase_ns = std::getenv("HPS_DEPHASE_NS") ? std::atoll(std::getenv("HPS_DEPHASE_NS")) : 0;
   DevBuf phase_buf;
   int store_e0 = -1, store_e1 = -1;
@@ -344,6 +347,7 @@ void enqueue_condense_chunk(hps_gpu_ctx* ctx, int e, int n, const double* d_b, c
   a.factor = 1;
   a.dephase_ns = ctx->dephase_ns;
   a.fused = ctx->fused ? 1 : 0;
+  a.lookahead = (ctx->lookahead && !ctx->fused) ? 1 : 0;
   a.rowcode = ctx->rowcode.as<int>();
   a.colcode = ctx->colcode.as<int>();
   a.Ds = ctx->Ds.as<double>();
@@ -366,6 +370,12 @@ void enqueue_condense_chunk(hps_gpu_ctx* ctx, int e, int n, const double* d_b, c
     double sum[8] = {0};
     for (int i = 0; i < n; ++i)
       for (int k = 0; k < 8; ++k) sum[k] += double(h[size_t(i) * 8 + k]);
+    if (a.lookahead)
+      std::fprintf(stderr,
+                   "[hps LA cycles/leaf] GEMM: wait-done %.3g window %.3g post-panel %.3g D-rows %.3g | "
+                   "panel: wait-ready %.3g work %.3g\n",
+                   sum[0] / n, sum[1] / n, sum[2] / n, sum[5] / n, sum[3] / n, sum[4] / n);
+    else
     std::fprintf(stderr,
                  "[hps phase cycles/leaf] U-part %.3g  L-part %.3g  panel %.3g (strips %.3g upd-U %.3g "
                  "upd-L %.3g)  linv %.3g  trailing %.3g\n",

@@ -41,6 +41,7 @@ struct LuArgs {
   int factor;           // 1: factor A_ii then trailing columns; 0: trailing columns only
   long long* phase_cycles = nullptr;  // optional 8 counters per leaf (profiling)
   long long dephase_ns = 0;           // start delay of the second CTA on each SM
+  int lookahead = 0;                  // condense: panel/GEMM warp-specialised kernel
   // Fused first-touch assembly (fused = 1): tile C-inits are evaluated from the
   // operator definition instead of loaded from a K1-materialised workspace.
   int fused = 0;

@@ -37,7 +37,7 @@ namespace hpsg {
 // 0 U-part tiles, 1 L-part tiles, 2 panel strips+updates, 3 Linv, 4 trailing.
 #define PHASE_MARK(slot)                                                     \
   do {                                                                       \
-    if (pc && threadIdx.x == 0) {                                            \
+    if (pc && G.tid == 0) {                                                  \
       const long long now__ = clock64();                                     \
       pc[slot] += now__ - t_phase;                                           \
       t_phase = now__;                                                       \
@@ -45,33 +45,45 @@ namespace hpsg {
   } while (0)
 
 constexpr int NT = 256;              // threads per CTA (8 warps, 32x32 warp tiles)
-#ifndef HPS_KC
-#define HPS_KC 16
-#endif
-#ifndef HPS_NSTAGE
-#define HPS_NSTAGE 3
-#endif
-constexpr int KC = HPS_KC;           // K chunk per pipeline stage
-constexpr int NSTAGE = HPS_NSTAGE;
-constexpr int LDA_S = KC + 4;        // 20 doubles: conflict-free A fragment loads
-constexpr int NSLOT = 8;             // strip rows per thread: R <= 2048 (p <= 45)
+constexpr int KC = 16;               // K chunk per stage (2-leaves-per-SM kernel)
+constexpr int NSTAGE = 3;            // stages (2-leaves-per-SM kernel)
+constexpr int MAX_NSTAGE = 4;
+constexpr int MAX_NSLOT = 8;         // strip rows per thread: R <= 2048 (p <= 45)
 constexpr int MAX_RPAD = 2048 + 128; // perm entries (tile gathers may run 127 past R)
+
+// A group of 256 threads (8 warps) sharing a named barrier.  The one-leaf-per-CTA kernel
+// uses the whole CTA (barrier 0); the lookahead kernel runs a GEMM group (threads 0-255,
+// barrier 1) and a panel group (threads 256-511, barrier 2) side by side.
+struct Grp {
+  int tid;   // thread index within the group
+  int bar;   // named barrier id
+  __device__ __forceinline__ void sync() const {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(bar), "r"(NT) : "memory");
+  }
+};
 
 // Tile jobs C(TM x TN) <- C -/+ A(TM x K) B(K x TN): 128x64 for the L part and the
 // D rows (row-tall), 64x128 for the U part (row-wide).  Stage: A TM x KC (+4 pad),
 // B KC x TN (+4 pad); both pads make the m8n8k4 fragment loads bank-conflict free.
-template <int TM_, int TN_>
+template <int TM_, int TN_, int KC_ = KC, int NS_ = NSTAGE>
 struct Tile {
   static constexpr int WM = TM_ / 32, WN = TN_ / 32;   // warp grid, WM * WN == 8
+  static constexpr int K = KC_;                       // K chunk
+  static constexpr int NS = NS_;                      // pipeline stages
+  static constexpr int LDA = KC_ + 4;                 // == 4 mod 16: conflict-free A fragments
   static constexpr int LDB = TN_ + 4;
-  static constexpr int STAGE = TM_ * LDA_S + KC * LDB;
-  static constexpr int AGR = TM_ * KC / 2 / NT;       // 16-byte A granules / thread / chunk
-  static constexpr int BGR = KC * TN_ / 2 / NT;       // 16-byte B granules / thread / chunk
+  static constexpr int STAGE = TM_ * LDA + KC_ * LDB;
+  static constexpr int AGR = TM_ * KC_ / 2 / NT;      // 16-byte A granules / thread / chunk
+  static constexpr int BGR = KC_ * TN_ / 2 / NT;      // 16-byte B granules / thread / chunk
   static constexpr int BROW = TN_ / 2;                // granules per B row
   static_assert(WM * WN == NT / 32, "8 warps");
+  static_assert(NS_ <= MAX_NSTAGE, "stages");
 };
 using TileL = Tile<128, 64>;
 using TileU = Tile<64, 128>;
+// Lookahead kernel (1 CTA/SM, more shared memory): 4 stages.
+using TileL2 = Tile<128, 64, 16, 4>;
+using TileU2 = Tile<64, 128, 16, 4>;
 constexpr int LS_U = 132;            // Linv-apply staging of a 64x128 U tile (== 4 mod 16)
 constexpr int cmax(int a, int b) { return a > b ? a : b; }
 constexpr int PIPE_DBL = cmax(cmax(NSTAGE * TileL::STAGE, NSTAGE * TileU::STAGE), 64 * LS_U);
@@ -114,14 +126,14 @@ template <class TL, class ARow, class BRow>
 __device__ __forceinline__ void load_chunk(double* st, unsigned long long* full, const double* const* pa,
                                            const ARow& arow, const BRow& brow, int k0, int K) {
   double* As = st;
-  double* Bs = st + (TL::WM * 32) * LDA_S;
+  double* Bs = st + (TL::WM * 32) * TL::LDA;
   const int tid = threadIdx.x;
-  constexpr int TM_ = TL::WM * 32, TN_ = TL::WN * 32;
-  if (k0 + KC <= K) {
+  constexpr int TM_ = TL::WM * 32, TN_ = TL::WN * 32, KC_ = TL::K;
+  if (k0 + KC_ <= K) {
 #pragma unroll
     for (int r = 0; r < TL::AGR; ++r) {
       const int gi = tid + r * NT;
-      cp_async16(As + (gi / (KC / 2)) * LDA_S + 2 * (gi % (KC / 2)), pa[r] + k0);
+      cp_async16(As + (gi / (KC_ / 2)) * TL::LDA + 2 * (gi % (KC_ / 2)), pa[r] + k0);
     }
 #pragma unroll
     for (int r = 0; r < TL::BGR; ++r) {
@@ -131,11 +143,11 @@ __device__ __forceinline__ void load_chunk(double* st, unsigned long long* full,
     }
     cp_async_mbar_arrive(full);
   } else {
-    for (int e = tid; e < TM_ * KC; e += NT) {
-      const int row = e / KC, col = e % KC;
-      As[row * LDA_S + col] = (k0 + col < K) ? arow(row)[k0 + col] : 0.0;
+    for (int e = tid; e < TM_ * KC_; e += NT) {
+      const int row = e / KC_, col = e % KC_;
+      As[row * TL::LDA + col] = (k0 + col < K) ? arow(row)[k0 + col] : 0.0;
     }
-    for (int e = tid; e < KC * TN_; e += NT) {
+    for (int e = tid; e < KC_ * TN_; e += NT) {
       const int row = e / TN_, col = e % TN_;
       Bs[row * TL::LDB + col] = (k0 + row < K) ? brow(k0 + row)[col] : 0.0;
     }
@@ -148,10 +160,11 @@ __device__ __forceinline__ void load_chunk(double* st, unsigned long long* full,
 // consumed) instead of a CTA-wide barrier per K chunk.  Chunks are numbered per CTA
 // (sm->gchunk) across tile jobs so the barrier phases stay consistent.
 template <class TL, class ARow, class BRow, class Init>
-__device__ void tile_mma(Acc& acc, const Init& init, const ARow& arow, const BRow& brow, int K,
-                         double sign, double* pipe, unsigned long long* full,
+__device__ void tile_mma(const Grp& G, Acc& acc, const Init& init, const ARow& arow, const BRow& brow,
+                         int K, double sign, double* pipe, unsigned long long* full,
                          unsigned long long* empty, unsigned* gchunk) {
-  const int nch = (K + KC - 1) / KC;
+  constexpr int KC_ = TL::K, NS_ = TL::NS;
+  const int nch = (K + KC_ - 1) / KC_;
   if (nch == 0) {
     init(acc);
     return;
@@ -164,30 +177,30 @@ __device__ void tile_mma(Acc& acc, const Init& init, const ARow& arow, const BRo
 #pragma unroll
   for (int r = 0; r < TL::AGR; ++r) {
     const int gi = threadIdx.x + r * NT;
-    pa[r] = arow(gi / (KC / 2)) + 2 * (gi % (KC / 2));
+    pa[r] = arow(gi / (KC_ / 2)) + 2 * (gi % (KC_ / 2));
   }
   auto fill = [&](int c) {
     const unsigned gf = g0 + c;
-    const int st = gf % NSTAGE;
-    if (gf >= NSTAGE) mbar_wait(&empty[st], ((gf - NSTAGE) / NSTAGE) & 1u);
-    load_chunk<TL>(pipe + st * TL::STAGE, &full[st], pa, arow, brow, c * KC, K);
+    const int st = gf % NS_;
+    if (gf >= NS_) mbar_wait(&empty[st], ((gf - NS_) / NS_) & 1u);
+    load_chunk<TL>(pipe + st * TL::STAGE, &full[st], pa, arow, brow, c * KC_, K);
   };
 #pragma unroll
-  for (int s = 0; s < NSTAGE - 1; ++s)
+  for (int s = 0; s < NS_ - 1; ++s)
     if (s < nch) fill(s);
   init(acc);   // C-init (load or first-touch assembly) overlaps the prologue copies
   for (int c = 0; c < nch; ++c) {
-    if (c + NSTAGE - 1 < nch) fill(c + NSTAGE - 1);
+    if (c + NS_ - 1 < nch) fill(c + NS_ - 1);
     const unsigned gc = g0 + c;
-    const int st = gc % NSTAGE;
-    mbar_wait(&full[st], (gc / NSTAGE) & 1u);
+    const int st = gc % NS_;
+    mbar_wait(&full[st], (gc / NS_) & 1u);
     const double* As = pipe + st * TL::STAGE;
-    const double* Bs = As + (TL::WM * 32) * LDA_S;
+    const double* Bs = As + (TL::WM * 32) * TL::LDA;
 #pragma unroll
-    for (int kk = 0; kk < KC / 4; ++kk) {
+    for (int kk = 0; kk < KC_ / 4; ++kk) {
       double a[4], b[4];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) a[mi] = sign * As[(32 * wm + 8 * mi + g) * LDA_S + 4 * kk + t];
+      for (int mi = 0; mi < 4; ++mi) a[mi] = sign * As[(32 * wm + 8 * mi + g) * TL::LDA + 4 * kk + t];
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) b[ni] = Bs[(4 * kk + t) * TL::LDB + 32 * wn + 8 * ni + g];
 #pragma unroll
@@ -198,9 +211,9 @@ __device__ void tile_mma(Acc& acc, const Init& init, const ARow& arow, const BRo
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
   }
-  __syncthreads();
-  if (threadIdx.x == 0) *gchunk = g0 + nch;
-  __syncthreads();
+  G.sync();
+  if (G.tid == 0) *gchunk = g0 + nch;
+  G.sync();
 }
 
 // C tile element access, rows masked by nrows, columns by ncols.
@@ -286,7 +299,8 @@ __device__ __forceinline__ void acc_store(const Acc& acc, const CRow& crow, int 
 // U-part epilogue: acc (64x128 tile) <- Linv (64x64) * acc.  The tile goes through
 // shared memory; Linv fragments come straight from global (32 KB per block row, L1/L2
 // resident across the block row's tiles).
-__device__ __forceinline__ void linv_apply(Acc& acc, const double* __restrict__ linv, double* pipe) {
+__device__ __forceinline__ void linv_apply(const Grp& G, Acc& acc, const double* __restrict__ linv,
+                                           double* pipe) {
   double* Cs = pipe;   // 64 x LS_U
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
@@ -294,7 +308,7 @@ __device__ __forceinline__ void linv_apply(Acc& acc, const double* __restrict__ 
     for (int ni = 0; ni < 4; ++ni)
       *reinterpret_cast<double2*>(Cs + acc_row<TileU>(mi) * LS_U + acc_col<TileU>(ni)) =
           make_double2(acc.v[mi][ni][0], acc.v[mi][ni][1]);
-  __syncthreads();
+  G.sync();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int wm = warp % TileU::WM, wn = warp / TileU::WM;
   acc_zero(acc);
@@ -302,7 +316,7 @@ __device__ __forceinline__ void linv_apply(Acc& acc, const double* __restrict__ 
   for (int kk = 0; kk < 16; ++kk) {
     double av[4], bv[4];
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi) av[mi] = __ldg(linv + (32 * wm + 8 * mi + g) * 64 + 4 * kk + t);
+    for (int mi = 0; mi < 4; ++mi) av[mi] = linv[(32 * wm + 8 * mi + g) * 64 + 4 * kk + t];  // coherent: Linv is written in-kernel
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) bv[ni] = Cs[(4 * kk + t) * LS_U + 32 * wn + 8 * ni + g];
 #pragma unroll
@@ -310,17 +324,20 @@ __device__ __forceinline__ void linv_apply(Acc& acc, const double* __restrict__ 
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) dmma(acc.v[mi][ni][0], acc.v[mi][ni][1], av[mi], bv[ni]);
   }
-  __syncthreads();
+  G.sync();
 }
 
 // ---------------------------------------------------------------------------
 // Panel factorisation pieces
 // ---------------------------------------------------------------------------
 struct LeafCtx {
-  double* M;         // leaf workspace
+  double* M;                 // leaf workspace
   int ld, R, ni;
-  short* perm;       // shared
-  Smem* sm;
+  short* perm;               // shared: logical -> physical
+  short* iperm;              // shared: physical -> logical
+  double* scratch;           // shared: panel scratch (>= 64*65 doubles)
+  double* wrow;              // shared: [2][8][4] pivot candidate rows
+  unsigned long long* redk;  // shared: [2][8] pivot keys
 };
 
 __device__ __forceinline__ double* mrow(const LeafCtx& L, int logical) {
@@ -341,9 +358,9 @@ __device__ __forceinline__ unsigned long long pivot_key(double v, int phys) {
          static_cast<unsigned long long>(0x7FF - phys);
 }
 
-__device__ void base_strip(const LeafCtx& L, int e, int sw, double& minpiv) {
-  Smem* sm = L.sm;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+template <int NSLOT>
+__device__ void base_strip(const Grp& G, const LeafCtx& L, int e, int sw, double& minpiv) {
+  const int tid = G.tid, lane = tid & 31, warp = tid >> 5;
   const int nrows = L.R - e;
   double x[NSLOT][4];
   int phys[NSLOT];
@@ -362,7 +379,7 @@ __device__ void base_strip(const LeafCtx& L, int e, int sw, double& minpiv) {
         if (j < sw) x[s][j] = src[j];
     }
   }
-  __syncthreads();  // all perm reads done before thread 0 starts swapping
+  G.sync();  // all perm reads done before thread 0 starts swapping
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     if (j >= sw) break;
@@ -382,39 +399,40 @@ __device__ void base_strip(const LeafCtx& L, int e, int sw, double& minpiv) {
       const unsigned long long ok = __shfl_xor_sync(0xffffffffu, wbest, o);
       wbest = ok > wbest ? ok : wbest;
     }
-    if (lane == 0) sm->redk[buf][warp] = wbest;
+    if (lane == 0) L.redk[buf * 8 + warp] = wbest;
     if (best == wbest && best != 0ull) {  // this lane owns the warp's candidate row
       double r0 = x[0][0], r1 = x[0][1], r2 = x[0][2], r3 = x[0][3];
 #pragma unroll
       for (int s = 1; s < NSLOT; ++s)
         if (s == bs) { r0 = x[s][0]; r1 = x[s][1]; r2 = x[s][2]; r3 = x[s][3]; }
-      sm->wrow[buf][warp][0] = r0;
-      sm->wrow[buf][warp][1] = r1;
-      sm->wrow[buf][warp][2] = r2;
-      sm->wrow[buf][warp][3] = r3;
+      double* wr = L.wrow + (buf * 8 + warp) * 4;
+      wr[0] = r0;
+      wr[1] = r1;
+      wr[2] = r2;
+      wr[3] = r3;
     }
-    __syncthreads();
-    unsigned long long kb = sm->redk[buf][0];
+    G.sync();
+    unsigned long long kb = L.redk[buf * 8];
     int ww = 0;
 #pragma unroll
     for (int w = 1; w < NT / 32; ++w) {
-      const unsigned long long k = sm->redk[buf][w];
+      const unsigned long long k = L.redk[buf * 8 + w];
       if (k > kb) { kb = k; ww = w; }
     }
     const int pphys = 0x7FF - static_cast<int>(kb & 0x7FFull);
     double prow[4];
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj) prow[jj] = sm->wrow[buf][ww][jj];
+    for (int jj = 0; jj < 4; ++jj) prow[jj] = L.wrow[(buf * 8 + ww) * 4 + jj];
     const double piv = prow[j];
     const double rpiv = 1.0 / piv;   // dgetf2-style reciprocal scaling
     if (tid == 0) {
       minpiv = fmin(minpiv, fabs(piv));
-      const int q = sm->iperm[pphys];
+      const int q = L.iperm[pphys];
       const int pold = L.perm[col];
       L.perm[col] = (short)pphys;
       L.perm[q] = (short)pold;
-      sm->iperm[pphys] = (short)col;
-      sm->iperm[pold] = (short)q;
+      L.iperm[pphys] = (short)col;
+      L.iperm[pold] = (short)q;
     }
 #pragma unroll
     for (int s = 0; s < NSLOT; ++s) {
@@ -437,7 +455,7 @@ __device__ void base_strip(const LeafCtx& L, int e, int sw, double& minpiv) {
       if (j < sw) dst[j] = x[s][j];
   }
   __threadfence_block();
-  __syncthreads();
+  G.sync();
 }
 
 constexpr int XS = 36;  // stride of the in-panel h x nd blocks (== 4 mod 16: conflict-free B fragments)
@@ -447,15 +465,14 @@ constexpr int XS = 36;  // stride of the in-panel h x nd blocks (== 4 mod 16: co
 //   U part (rows s0..s0+h-1):  X = L_hh^{-1} X     one warp, column per lane, no barriers
 //   L part (rows d0..R-1)   :  C -= A[:, src] X    DMMA m8n8k4, one 8-row group per warp
 template <int H>
-__device__ void panel_update_t(const LeafCtx& L, int s0, int d0, int nd, long long* pc,
+__device__ void panel_update_t(const Grp& G, const LeafCtx& L, int s0, int d0, int nd, long long* pc,
                                long long& t_phase) {
   constexpr int NTILE = (H + 7) / 8;        // 8-wide DMMA column tiles (nd <= H)
   constexpr int UNR = H <= 8 ? 4 : 2;       // 8-row groups in flight per warp
   constexpr int KS = H / 4;                 // DMMA k-steps
-  Smem* sm = L.sm;
-  double* Ls = sm->pipe;               // H x H   (stride XS)
-  double* X = sm->pipe + 32 * XS;      // H x 8*NTILE (stride XS), zero padded
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* Ls = L.scratch;              // H x H   (stride XS)
+  double* X = L.scratch + 32 * XS;     // H x 8*NTILE (stride XS), zero padded
+  const int tid = G.tid, lane = tid & 31, warp = tid >> 5;
   for (int e = tid; e < H * H; e += NT) {
     const int i = e / H, k = e % H;
     Ls[i * XS + k] = (k < i) ? mrow(L, s0 + i)[s0 + k] : 0.0;
@@ -464,7 +481,7 @@ __device__ void panel_update_t(const LeafCtx& L, int s0, int d0, int nd, long lo
     const int i = e / (8 * NTILE), j = e % (8 * NTILE);
     X[i * XS + j] = j < nd ? mrow(L, s0 + i)[d0 + j] : 0.0;
   }
-  __syncthreads();
+  G.sync();
   if (warp == 0 && lane < nd) {  // U part: one column per lane, registers, no barriers
     double x[H];
 #pragma unroll
@@ -476,7 +493,7 @@ __device__ void panel_update_t(const LeafCtx& L, int s0, int d0, int nd, long lo
 #pragma unroll
     for (int i = 0; i < H; ++i) X[i * XS + lane] = x[i];
   }
-  __syncthreads();
+  G.sync();
   for (int e = tid; e < H * nd; e += NT) {
     const int i = e / nd, j = e % nd;
     mrow(L, s0 + i)[d0 + j] = X[i * XS + j];
@@ -527,7 +544,7 @@ __device__ void panel_update_t(const LeafCtx& L, int s0, int d0, int nd, long lo
     }
   }
   __threadfence_block();
-  __syncthreads();
+  G.sync();
   PHASE_MARK(7);
 }
 
@@ -535,13 +552,13 @@ __device__ void panel_update_t(const LeafCtx& L, int s0, int d0, int nd, long lo
 // destination columns [d0, d0+nd) (d0 = s0+h) carry all earlier updates.
 //   U part (rows s0..s0+h-1):  X = L_hh^{-1} X     one warp, column per lane, registers
 //   L part (rows d0..R-1)   :  C -= A[:, src] X    DMMA m8n8k4 over 8-row groups
-__device__ void panel_update(const LeafCtx& L, int s0, int h, int d0, int nd, long long* pc,
-                             long long& t_phase) {
+__device__ void panel_update(const Grp& G, const LeafCtx& L, int s0, int h, int d0, int nd,
+                             long long* pc, long long& t_phase) {
   switch (h) {
-    case 4: panel_update_t<4>(L, s0, d0, nd, pc, t_phase); break;
-    case 8: panel_update_t<8>(L, s0, d0, nd, pc, t_phase); break;
-    case 16: panel_update_t<16>(L, s0, d0, nd, pc, t_phase); break;
-    default: panel_update_t<32>(L, s0, d0, nd, pc, t_phase); break;
+    case 4: panel_update_t<4>(G, L, s0, d0, nd, pc, t_phase); break;
+    case 8: panel_update_t<8>(G, L, s0, d0, nd, pc, t_phase); break;
+    case 16: panel_update_t<16>(G, L, s0, d0, nd, pc, t_phase); break;
+    default: panel_update_t<32>(G, L, s0, d0, nd, pc, t_phase); break;
   }
 }
 
@@ -549,47 +566,44 @@ __device__ void panel_update(const LeafCtx& L, int s0, int h, int d0, int nd, lo
 // identity-padded, row-major).  Warp w owns columns 8w..8w+7; the four lanes of a
 // column hold 16 rows each in registers and step through k with a shuffle
 // broadcast of X[k][j] -- no block barriers inside.
-__device__ void panel_linv(const LeafCtx& L, int c0, int w, double* linv) {
-  double* Ls = L.sm->pipe;            // 64 x 65
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+__device__ void panel_linv(const Grp& G, const LeafCtx& L, int c0, int w, double* linv) {
+  double* Ls = L.scratch;             // 64 x 65
+  const int tid = G.tid, lane = tid & 31, warp = tid >> 5;
   for (int e = tid; e < 64 * 64; e += NT) {
     const int i = e >> 6, k = e & 63;
     Ls[i * 65 + k] = (i < w && k < i) ? mrow(L, c0 + i)[c0 + k] : 0.0;
   }
-  __syncthreads();
+  G.sync();
+  // lane (jj, q): column j = 8 warp + jj, rows i = 4 r + q (r < 16).  Rows interleaved by
+  // quarter so the four quarters' Ls reads hit four different banks.
   const int j = 8 * warp + (lane >> 2), q = lane & 3;
   double x[16];
 #pragma unroll
-  for (int r = 0; r < 16; ++r) x[r] = (16 * q + r == j) ? 1.0 : 0.0;
+  for (int r = 0; r < 16; ++r) x[r] = (4 * r + q == j) ? 1.0 : 0.0;
 #pragma unroll
-  for (int qo = 0; qo < 4; ++qo) {
+  for (int k = 0; k < 63; ++k) {
+    const double xk = __shfl_sync(0xffffffffu, x[k >> 2], (lane & ~3) | (k & 3));
 #pragma unroll
-    for (int kk = 0; kk < 16; ++kk) {
-      const int k = 16 * qo + kk;
-      const double xk = __shfl_sync(0xffffffffu, x[kk], (lane & ~3) | qo);
-      if (q >= qo) {
-#pragma unroll
-        for (int r = 0; r < 16; ++r)
-          if (16 * q + r > k) x[r] = fma(-Ls[(16 * q + r) * 65 + k], xk, x[r]);
-      }
-    }
+    for (int r = 0; r < 16; ++r)
+      if (4 * r + q > k) x[r] = fma(-Ls[(4 * r + q) * 65 + k], xk, x[r]);
   }
 #pragma unroll
-  for (int r = 0; r < 16; ++r) linv[(16 * q + r) * 64 + j] = x[r];
-  __syncthreads();
+  for (int r = 0; r < 16; ++r) linv[(4 * r + q) * 64 + j] = x[r];
+  G.sync();
 }
 
-__device__ void panel_factor(const LeafCtx& L, int c0, int w, double& minpiv, long long* pc,
-                             long long& t_phase) {
+template <int NSLOT>
+__device__ void panel_factor(const Grp& G, const LeafCtx& L, int c0, int w, double& minpiv,
+                             long long* pc, long long& t_phase) {
   for (int e = c0; e < c0 + w;) {
     const int sw = min(4, c0 + w - e);
-    base_strip(L, e, sw, minpiv);
+    base_strip<NSLOT>(G, L, e, sw, minpiv);
     PHASE_MARK(5);
     e += sw;
     const int done = e - c0;
     if (done < w) {
       const int h = done & (-done);      // lowest set bit: recursive-LU schedule
-      panel_update(L, e - h, h, e, min(h, c0 + w - e), pc, t_phase);
+      panel_update(G, L, e - h, h, e, min(h, c0 + w - e), pc, t_phase);
     }
   }
 }
@@ -597,7 +611,9 @@ __device__ void panel_factor(const LeafCtx& L, int c0, int w, double& minpiv, lo
 // ---------------------------------------------------------------------------
 // Kernel
 // ---------------------------------------------------------------------------
+template <int NSLOT>
 __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
+  const Grp G{(int)threadIdx.x, 0};
   const LeafDims d = a.d;
   LeafCtx L;
   L.M = a.ws + (size_t)leaf * d.leaf_stride;
@@ -605,7 +621,10 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
   L.R = d.R;
   L.ni = d.ni;
   L.perm = sm->perm;
-  L.sm = sm;
+  L.iperm = sm->iperm;
+  L.scratch = sm->pipe;
+  L.wrow = &sm->wrow[0][0][0];
+  L.redk = &sm->redk[0][0];
   double* Linv = a.linv + (size_t)leaf * d.nblk * 4096;
   short* perm_g = a.perm + (size_t)leaf * d.Rpad;
   // Entries past Rpad are read by masked-out tile rows (e.g. the D-row tiles start at ni, which
@@ -614,7 +633,7 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
     sm->perm[i] = i < d.Rpad ? (a.factor ? (short)i : perm_g[i]) : (short)(d.Rpad - 1);
     sm->iperm[i] = (short)i;   // only used while factoring (perm starts as the identity)
   }
-  __syncthreads();
+  G.sync();
   double minpiv = INFINITY;  // meaningful on thread 0
   long long* pc = a.phase_cycles ? a.phase_cycles + (size_t)leaf * 8 : nullptr;
   Orig orig;
@@ -656,15 +675,15 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
         };
         auto arow = lrow(rt);
         auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + c0; };
-        tile_mma<TileL>(acc, init, arow, brow, c0, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
+        tile_mma<TileL>(G, acc, init, arow, brow, c0, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
         acc_store<TileL>(acc, crow, nr, 64);
       }
       __threadfence_block();
-      __syncthreads();
+      G.sync();
       PHASE_MARK(1);
-      panel_factor(L, c0, w, minpiv, pc, t_phase);
+      panel_factor<NSLOT>(G, L, c0, w, minpiv, pc, t_phase);
       PHASE_MARK(2);
-      panel_linv(L, c0, w, Linv + (size_t)J * 4096);
+      panel_linv(G, L, c0, w, Linv + (size_t)J * 4096);
       PHASE_MARK(3);
     }
     const double* li = Linv + (size_t)J * 4096;
@@ -679,12 +698,12 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
       };
       auto arow = lrow(c0);
       auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + ct; };
-      tile_mma<TileU>(acc, init, arow, brow, c0, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
-      linv_apply(acc, li, sm->pipe);
+      tile_mma<TileU>(G, acc, init, arow, brow, c0, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
+      linv_apply(G, acc, li, sm->pipe);
       acc_store<TileU>(acc, crow, w, min(128, ct_end - ct));
     }
     __threadfence_block();
-    __syncthreads();
+    G.sync();
     PHASE_MARK(0);
   }
 
@@ -704,7 +723,7 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
       };
       auto arow = lrow(rt);
       auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + c0; };
-      tile_mma<TileL>(acc, init, arow, brow, d.ni, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
+      tile_mma<TileL>(G, acc, init, arow, brow, d.ni, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi) {
         const int r = acc_row<TileL>(mi);
@@ -722,13 +741,13 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
       }
     }
   }
-  __syncthreads();
+  G.sync();
   PHASE_MARK(4);
   if (!a.factor) {
-    __syncthreads();
+    G.sync();
     return;
   }
-  __syncthreads();
+  G.sync();
   for (int i = threadIdx.x; i < d.Rpad; i += NT) perm_g[i] = sm->perm[i];
   if (threadIdx.x == 0) {
     const double nrm = a.norms[leaf];
@@ -736,13 +755,14 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
     if (a.minratio) a.minratio[leaf] = ratio;
     a.status[leaf] = (ratio >= 1e-12) ? 0 : 1;
   }
-  __syncthreads();
+  G.sync();
 }
 
 // Persistent: grid = 2 CTAs per SM, each walks leaves blockIdx.x, +gridDim.x, ...
 // The second CTA of every SM (blockIdx >= gridDim/2; classic placement puts b and
 // b + #SM on one SM) starts `dephase_ns` late so the two co-resident leaves are not in
 // their (latency-bound) panel phases at the same time.
+template <int NSLOT>
 __global__ void __launch_bounds__(NT, 2) k2_lu_schur_kernel(LuArgs a, int n_leaves) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem* sm = reinterpret_cast<Smem*>(smem_raw);
@@ -758,20 +778,265 @@ __global__ void __launch_bounds__(NT, 2) k2_lu_schur_kernel(LuArgs a, int n_leav
     const long long t0 = globaltimer();
     while (globaltimer() - t0 < a.dephase_ns) __nanosleep(20000);
   }
-  for (int leaf = blockIdx.x; leaf < n_leaves; leaf += gridDim.x) process_leaf(a, sm, leaf);
+  for (int leaf = blockIdx.x; leaf < n_leaves; leaf += gridDim.x) process_leaf<NSLOT>(a, sm, leaf);
+}
+
+// ===========================================================================
+// Lookahead kernel: one CTA (16 warps) per SM and leaf.  Warps 0-7 (GEMM group) run all
+// tile jobs; warps 8-15 (panel group) factor panel J while the GEMM group works on what
+// does not depend on it:
+//   window of panel J : U(J-1, c >= J+1)                      (block row J-1, Linv epilogue)
+//                       partial L(J+1), K in [0, c0_J), on the rows not pivoted before
+//                       panel J (perm snapshot) -- this also pre-computes A - L U for
+//                       the rows that become panel J's pivot rows
+//   after panel J     : U(J, J+1) = Linv_J * partial           (no GEMM, Linv only)
+//                       L(J+1) remainder, K = block J (64)      -> panel J+1 may start
+// Hand-offs are two mbarriers (GEMM -> panel "column ready", panel -> GEMM "panel done").
+// Each output element is computed by the same tile code as in k2_lu_schur_kernel; only the
+// split of K between the partial and the remainder pass differs for the L part.
+// ===========================================================================
+constexpr int NT_LA = 2 * NT;
+constexpr int PAN_DBL = 64 * 65;
+constexpr int PIPE_LA = cmax(cmax(TileL2::NS * TileL2::STAGE, TileU2::NS * TileU2::STAGE), 64 * LS_U);
+
+struct SmemLA {
+  double pipe[PIPE_LA];
+  double pan[PAN_DBL];
+  double wrow[2][NT / 32][4];
+  unsigned long long redk[2][NT / 32];
+  unsigned long long full[MAX_NSTAGE];
+  unsigned long long empty[MAX_NSTAGE];
+  unsigned long long ready_bar;   // GEMM -> panel: column J fully updated
+  unsigned long long done_bar;    // panel -> GEMM: panel J + Linv_J done
+  unsigned gchunk;
+  short perm[MAX_RPAD];
+  short iperm[MAX_RPAD];
+  short snap[MAX_RPAD];           // perm snapshot: candidate rows of the running panel
+};
+
+__device__ __forceinline__ void group_release(const Grp& G, unsigned long long* bar) {
+  __threadfence_block();
+  G.sync();
+  if (G.tid == 0) mbar_arrive(bar);
+}
+
+template <int NSLOT>
+__device__ void process_leaf_la(const LuArgs& a, SmemLA* sm, const int leaf, const unsigned pbase) {
+  const LeafDims d = a.d;
+  const bool gemm = threadIdx.x < NT;
+  const Grp G{gemm ? (int)threadIdx.x : (int)threadIdx.x - NT, gemm ? 1 : 2};
+  double* Mw = a.ws + (size_t)leaf * d.leaf_stride;
+  double* Linv = a.linv + (size_t)leaf * d.nblk * 4096;
+  const int ld = d.ld;
+  for (int i = threadIdx.x; i < MAX_RPAD; i += NT_LA) {
+    const short v = i < d.Rpad ? (short)i : (short)(d.Rpad - 1);
+    sm->perm[i] = v;
+    sm->snap[i] = v;
+    sm->iperm[i] = (short)i;
+  }
+  __syncthreads();
+  // optional timers (thread 0 of each group): GEMM 0 wait-done 1 window 2 post-panel 5 D rows;
+  // panel 3 wait-ready 4 factor+linv
+  long long* pcl = a.phase_cycles ? a.phase_cycles + (size_t)leaf * 8 : nullptr;
+  long long* pc = nullptr;      // (in-panel sub-phase marks off)
+  long long t_phase = 0;
+  long long tl = clock64();
+  auto mark = [&](int slot) {
+    if (pcl && G.tid == 0) {
+      const long long now = clock64();
+      pcl[slot] += now - tl;
+      tl = now;
+    }
+  };
+
+  if (!gemm) {
+    // ------------------------------ panel group ------------------------------
+    LeafCtx L;
+    L.M = Mw;
+    L.ld = ld;
+    L.R = d.R;
+    L.ni = d.ni;
+    L.perm = sm->perm;
+    L.iperm = sm->iperm;
+    L.scratch = sm->pan;
+    L.wrow = &sm->wrow[0][0][0];
+    L.redk = &sm->redk[0][0];
+    double minpiv = INFINITY;
+    for (int J = 0; J < d.nblk; ++J) {
+      const int c0 = 64 * J, w = min(64, d.ni - c0);
+      mark(4);
+      mbar_wait_sleep(&sm->ready_bar, (pbase + J) & 1u);
+      mark(3);
+      panel_factor<NSLOT>(G, L, c0, w, minpiv, pc, t_phase);
+      panel_linv(G, L, c0, w, Linv + (size_t)J * 4096);
+      group_release(G, &sm->done_bar);
+    }
+    if (G.tid == 0) {
+      const double nrm = a.norms[leaf];
+      const double ratio = nrm > 0.0 ? minpiv / nrm : 0.0;
+      if (a.minratio) a.minratio[leaf] = ratio;
+      a.status[leaf] = (ratio >= 1e-12) ? 0 : 1;
+    }
+  } else {
+    // ------------------------------ GEMM group -------------------------------
+    const double* M = Mw;
+    const short* perm = sm->perm;
+    const short* snap = sm->snap;
+    const int ct_end = d.tb0 + 64 * d.ntb;
+    auto utile = [&](int J, int ct, int K, int ncols) {   // U(J, ct..): full GEMM + Linv_J
+      const int c0 = 64 * J, w = min(64, d.ni - c0);
+      auto crow = [=](int i) -> double* { return Mw + (size_t)perm[c0 + i] * ld + ct; };
+      auto arow = [=](int i) -> const double* { return M + (size_t)perm[c0 + i] * ld; };
+      auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + ct; };
+      Acc acc;
+      auto init = [&](Acc& x) { acc_load<TileU2>(x, crow, 64); };
+      tile_mma<TileU2>(G, acc, init, arow, brow, K, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
+      linv_apply(G, acc, Linv + (size_t)J * 4096, sm->pipe);
+      acc_store<TileU2>(acc, crow, w, ncols);
+    };
+    // column 0 holds original values: panel 0 may start at once
+    group_release(G, &sm->ready_bar);
+    for (int J = 0; J < d.nblk; ++J) {
+      const int c0 = 64 * J;
+      // ---- window of panel J ----
+      if (J >= 1)
+        for (int ct = c0 + 64; ct < ct_end; ct += 128) utile(J - 1, ct, c0 - 64, min(128, ct_end - ct));
+      if (J + 1 < d.nblk && c0 > 0) {   // partial L(J+1): rows of the snapshot, K = c0
+        const int c1 = c0 + 64;
+        for (int rt = c0; rt < d.R; rt += 128) {
+          const int nr = min(128, d.R - rt);
+          auto crow = [=](int i) -> double* { return Mw + (size_t)snap[rt + i] * ld + c1; };
+          auto arow = [=](int i) -> const double* { return M + (size_t)snap[rt + i] * ld; };
+          auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + c1; };
+          Acc acc;
+          auto init = [&](Acc& x) { acc_load<TileL2>(x, crow, nr); };
+          tile_mma<TileL2>(G, acc, init, arow, brow, c0, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
+          acc_store<TileL2>(acc, crow, nr, 64);
+        }
+      }
+      mark(1);
+      mbar_wait_sleep(&sm->done_bar, (pbase + J) & 1u);
+      mark(0);
+      // ---- after panel J ----
+      if (J + 1 < d.nblk) {
+        const int c1 = c0 + 64;
+        {   // U(J, J+1) = Linv_J * (partial values of the pivot rows)
+          auto crow = [=](int i) -> double* { return Mw + (size_t)perm[c0 + i] * ld + c1; };
+          Acc acc;
+          acc_load<TileU2>(acc, crow, 64);
+          linv_apply(G, acc, Linv + (size_t)J * 4096, sm->pipe);
+          acc_store<TileU2>(acc, crow, 64, 64);
+        }
+        __threadfence_block();
+        G.sync();
+        // L(J+1) remainder: rows [c1, R), K = block J
+        for (int rt = c1; rt < d.R; rt += 128) {
+          const int nr = min(128, d.R - rt);
+          auto crow = [=](int i) -> double* { return Mw + (size_t)perm[rt + i] * ld + c1; };
+          auto arow = [=](int i) -> const double* { return M + (size_t)perm[rt + i] * ld + c0; };
+          auto brow = [=](int k) -> const double* { return M + (size_t)perm[c0 + k] * ld + c1; };
+          Acc acc;
+          auto init = [&](Acc& x) { acc_load<TileL2>(x, crow, nr); };
+          tile_mma<TileL2>(G, acc, init, arow, brow, 64, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
+          acc_store<TileL2>(acc, crow, nr, 64);
+        }
+        // snapshot the candidate rows of panel J+1 for the next partial pass
+        for (int i = c1 + G.tid; i < d.Rpad; i += NT) sm->snap[i] = sm->perm[i];
+        group_release(G, &sm->ready_bar);
+      } else {
+        // last panel: U(J, trailing) with the full K = c0
+        for (int ct = d.tb0; ct < ct_end; ct += 128) utile(J, ct, c0, min(128, ct_end - ct));
+        __threadfence_block();
+        G.sync();
+      }
+      mark(2);
+    }
+    // D rows of the trailing columns: T = D_b - L21 U12 ; -w = -L21 (L^{-1} f)  (K = ni)
+    double* Tl = a.T_out + (size_t)leaf * d.nb * d.nb;
+    double* wl = a.w_out + (size_t)leaf * d.nb;
+    for (int tb = 0; tb < d.ntb; ++tb) {
+      const int c0 = d.tb0 + 64 * tb;
+      for (int rt = d.ni; rt < d.R; rt += 128) {
+        const int nr = min(128, d.R - rt);
+        auto crow = [=](int i) -> double* { return Mw + (size_t)perm[rt + i] * ld + c0; };
+        auto arow = [=](int i) -> const double* { return M + (size_t)perm[rt + i] * ld; };
+        auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + c0; };
+        Acc acc;
+        auto init = [&](Acc& x) { acc_load<TileL2>(x, crow, nr); };
+        tile_mma<TileL2>(G, acc, init, arow, brow, d.ni, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi) {
+          const int r = acc_row<TileL2>(mi);
+          if (r >= nr) continue;
+          const int trow = rt + r - d.ni;
+#pragma unroll
+          for (int ni2 = 0; ni2 < 4; ++ni2) {
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const int tc = 64 * tb + acc_col<TileL2>(ni2) + hh;
+              if (tc < d.nb) Tl[(size_t)trow * d.nb + tc] = acc.v[mi][ni2][hh];
+              else if (tc == d.nb) wl[trow] = -acc.v[mi][ni2][hh];
+            }
+          }
+        }
+      }
+    }
+    mark(5);
+  }
+  __syncthreads();
+  short* perm_g = a.perm + (size_t)leaf * d.Rpad;
+  for (int i = threadIdx.x; i < d.Rpad; i += NT_LA) perm_g[i] = sm->perm[i];
+  __syncthreads();
+}
+
+template <int NSLOT>
+__global__ void __launch_bounds__(NT_LA, 1) k2_lu_lookahead_kernel(LuArgs a, int n_leaves) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SmemLA* sm = reinterpret_cast<SmemLA*>(smem_raw);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < MAX_NSTAGE; ++s) {
+      mbar_init(&sm->full[s], NT);
+      mbar_init(&sm->empty[s], NT / 32);
+    }
+    mbar_init(&sm->ready_bar, 1);
+    mbar_init(&sm->done_bar, 1);
+    sm->gchunk = 0;
+  }
+  __syncthreads();
+  unsigned pbase = 0;   // panels completed by this CTA (mbarrier phase base)
+  for (int leaf = blockIdx.x; leaf < n_leaves; leaf += gridDim.x) {
+    process_leaf_la<NSLOT>(a, sm, leaf, pbase);
+    pbase += a.d.nblk;
+  }
 }
 
 size_t lu_smem_bytes() { return sizeof(Smem); }
 
-void launch_lu_schur(const LuArgs& a, int n_leaves, cudaStream_t st) {
-  if (n_leaves <= 0) return;
-  cudaFuncSetAttribute(k2_lu_schur_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sizeof(Smem));
+template <int NSLOT>
+static void launch_ns(const LuArgs& a, int n_leaves, cudaStream_t st) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (a.lookahead && a.factor && a.d.nb > 0) {
+    cudaFuncSetAttribute(k2_lu_lookahead_kernel<NSLOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(SmemLA));
+    const int grid = n_leaves < sms ? n_leaves : sms;
+    k2_lu_lookahead_kernel<NSLOT><<<grid, NT_LA, sizeof(SmemLA), st>>>(a, n_leaves);
+    return;
+  }
+  cudaFuncSetAttribute(k2_lu_schur_kernel<NSLOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(Smem));
   const int grid = n_leaves < 2 * sms ? n_leaves : 2 * sms;
-  k2_lu_schur_kernel<<<grid, NT, sizeof(Smem), st>>>(a, n_leaves);
+  k2_lu_schur_kernel<NSLOT><<<grid, NT, sizeof(Smem), st>>>(a, n_leaves);
+}
+
+// Strip rows per thread = ceil(R / 256): register-resident pivot strips sized to p.
+void launch_lu_schur(const LuArgs& a, int n_leaves, cudaStream_t st) {
+  if (n_leaves <= 0) return;
+  const int need = (a.d.R + NT - 1) / NT;
+  if (need <= 2) launch_ns<2>(a, n_leaves, st);
+  else if (need <= 4) launch_ns<4>(a, n_leaves, st);
+  else launch_ns<8>(a, n_leaves, st);
 }
 
 }  // namespace hpsg

@@ -81,6 +81,7 @@ struct CondensedLeaf {
   int n_b = 0;
   std::vector<double> T_flux;   // n_b x n_b row-major
   std::vector<double> w_equiv;  // n_b
+  std::vector<double> S_solve;  // n_i x n_b row-major, -A_ii^{-1} A_ib (LeafStageConfig::want_s_solve)
 };
 
 // ReducedSystem in CSR over MeshTopology::active_of_global order.
@@ -99,6 +100,7 @@ struct LeafStageConfig {
   StoragePolicy storage = StoragePolicy::Recompute;  // SPEC.md:313 default
   int64_t workspace_bytes = 0;                       // 0: 70% of free HBM
   int workers = 0;                                   // host sampling threads (parallel.hpp semantics)
+  bool want_s_solve = false;                         // also return S_solve (K3 back substitution)
 };
 
 // One GPU context for one mesh/problem.  Not reentrant (one host thread per ctx).

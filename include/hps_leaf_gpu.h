@@ -90,7 +90,8 @@ int hps_gpu_reset_timing(hps_gpu_ctx* ctx);
 
 /* batched_condense (per leaf condense_leaf :279-287) for
  * elements [e0, e1).  Inputs b, f are the (e1-e0) leaves' samples (host).
- * Outputs (host, caller-owned): T (T_flux), w (w_equiv), S (S_solve, nullable),
+ * Outputs (host, caller-owned): T (T_flux), w (w_equiv), S (S_solve, nullable: when
+ * given, K3 back-substitutes -A_ii^{-1} A_ib from the factors, n_i x n_b per leaf),
  * status (0 ok / 1 resonance).  Returns HPS_ERR_RESONANCE if any leaf failed;
  * the message names the smallest failing element id and all failing ids. */
 int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, const double* f,

@@ -154,8 +154,11 @@ std::vector<CondensedLeaf> LeafStage::batched_condense(const std::vector<double>
   sample(0, n, f_full, b, f);
   double* T = static_cast<double*>(hps_host_alloc(sizeof(double) * size_t(n) * nb * nb));
   double* w = static_cast<double*>(hps_host_alloc(sizeof(double) * size_t(n) * nb));
+  const int ni = (topo_.params.p - 2) * (topo_.params.p - 2);
+  std::vector<double> S(cfg_.want_s_solve ? size_t(n) * ni * nb : 0);
   std::vector<int32_t> st(n);
-  const int rc = hps_gpu_condense(ctx_, 0, n, b.data(), f.data(), T, w, nullptr, st.data());
+  const int rc = hps_gpu_condense(ctx_, 0, n, b.data(), f.data(), T, w,
+                                  cfg_.want_s_solve ? S.data() : nullptr, st.data());
   std::vector<CondensedLeaf> out;
   if (rc == HPS_OK) {
     out.resize(n);
@@ -164,6 +167,8 @@ std::vector<CondensedLeaf> LeafStage::batched_condense(const std::vector<double>
       out[e].n_b = nb;
       out[e].T_flux.assign(T + size_t(e) * nb * nb, T + size_t(e + 1) * nb * nb);
       out[e].w_equiv.assign(w + size_t(e) * nb, w + size_t(e + 1) * nb);
+      if (cfg_.want_s_solve)
+        out[e].S_solve.assign(S.begin() + size_t(e) * ni * nb, S.begin() + size_t(e + 1) * ni * nb);
     }
   }
   hps_host_free(T);

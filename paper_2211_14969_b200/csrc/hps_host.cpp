@@ -196,7 +196,7 @@ struct hps_gpu_ctx {
   double k2 = 0.0;
   DevBuf rowcode, colcode, rowcode_s, colcode_s, Ds, D2;
   DevBuf ws, linv, perm, norms, minratio, status, inject_all;
-  DevBuf in_b[2], in_f[2], in_v[2], out_T[2], out_w[2], out_st[2], out_u[2];
+  DevBuf in_b[2], in_f[2], in_v[2], out_T[2], out_w[2], out_st[2], out_u[2], out_S[2], uinv;
   MeshHost mesh;
   DevBuf m_elem_edges, m_edge_elems, m_edge_sides, m_edge_cols, m_edge_ne, m_edge_off;
   cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr;
@@ -577,7 +577,6 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
                      double* T, double* w, double* S, int32_t* status) {
   if (!ctx) return HPS_ERR_PARAM;
   if (int rc = check_range(ctx, e0, e1)) return rc;
-  if (S) return ctx->fail(HPS_ERR_PARAM, "ParameterError: S_solve output is not available in this build");
   if (!b || !f || !T || !w || !status) return ctx->fail(HPS_ERR_PARAM, "ParameterError: null buffer");
   if (ctx->desc.storage == HPS_STORAGE_STORE && (e1 - e0) > ctx->chunk)
     return ctx->fail(HPS_ERR_PARAM, "ParameterError: store policy range exceeds resident factors");
@@ -591,7 +590,10 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
     CK(ctx->out_T[i].ensure(size_t(chunk) * nb2 * 8));
     CK(ctx->out_w[i].ensure(size_t(chunk) * d.nb * 8));
     CK(ctx->out_st[i].ensure(size_t(chunk) * 4));
+    if (S) CK(ctx->out_S[i].ensure(size_t(chunk) * d.ni * d.nb * 8));
   }
+  if (S) CK(ctx->uinv.ensure(size_t(2 * ctx->sms) * 4096 * 8));
+  const size_t nis = size_t(d.ni) * d.nb;
   reset_timing(ctx);
   int ci = 0;
   for (int c0 = e0; c0 < e1; c0 += chunk, ++ci) {
@@ -607,6 +609,14 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
     enqueue_condense_chunk(ctx, c0, n, ctx->in_b[k].as<double>(), ctx->in_f[k].as<double>(),
                            ctx->out_T[k].as<double>(), ctx->out_w[k].as<double>(),
                            ctx->out_st[k].as<int>(), ctx->s_comp);
+    if (S) {  // K3: S_solve from the factored workspace
+      hpsg::LuArgs a3;
+      a3.d = d;
+      a3.ws = ctx->ws.as<double>();
+      a3.perm = ctx->perm.as<short>();
+      hpsg::launch_ssolve(a3, ctx->out_S[k].as<double>(), ctx->uinv.as<double>(), n, ctx->s_comp);
+      ctx->tkernels += 1;
+    }
     CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev_in_free[k], ctx->s_comp));
     CK(cudaEventRecord(ctx->ev_out_ready[k], ctx->s_comp));
@@ -615,6 +625,8 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
     CK(cudaMemcpyAsync(w + off * d.nb, ctx->out_w[k].ptr, n * size_t(d.nb) * 8, cudaMemcpyDeviceToHost,
                        ctx->s_d2h));
     CK(cudaMemcpyAsync(status + off, ctx->out_st[k].ptr, n * 4, cudaMemcpyDeviceToHost, ctx->s_d2h));
+    if (S)
+      CK(cudaMemcpyAsync(S + off * nis, ctx->out_S[k].ptr, n * nis * 8, cudaMemcpyDeviceToHost, ctx->s_d2h));
     CK(cudaEventRecord(ctx->ev_out_free[k], ctx->s_d2h));
   }
   CK(cudaStreamSynchronize(ctx->s_d2h));

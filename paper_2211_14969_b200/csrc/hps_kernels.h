@@ -55,6 +55,9 @@ struct LuArgs {
   const int* inject = nullptr;         // per leaf, nullable
 };
 size_t lu_smem_bytes();
+// K3: S_solve = -A_ii^{-1} A_ib from a factored workspace (after K2).  uinv_ws: 4096
+// doubles per resident CTA (2 per SM).
+void launch_ssolve(const LuArgs& a, double* S_out, double* uinv_ws, int n_leaves, cudaStream_t st);
 void launch_lu_schur(const LuArgs& a, int n_leaves, cudaStream_t st);
 
 // K5: back substitution u_i = U^{-1} y (y = L^{-1} P rhs in column tb0) and the

@@ -1012,6 +1012,101 @@ __global__ void __launch_bounds__(NT_LA, 1) k2_lu_lookahead_kernel(LuArgs a, int
 
 size_t lu_smem_bytes() { return sizeof(Smem); }
 
+// ===========================================================================
+// K3 (standalone): S_solve = -A_ii^{-1} A_ib = -U^{-1} (L^{-1} P A_ib)
+// Runs after K2 on the same workspace.  Blocked back substitution over the 64-row blocks
+// of U, last to first:  X_I = Uinv_I (Y_I - U[I, >I] X_{>I}),  X stored in place of Y
+// (row k of X at the physical row of logical row k).  Uinv_I (upper, non-unit 64x64) is
+// formed warp-synchronously like Linv; the GEMM and the Uinv product reuse the K2 tile
+// code (64x128 tiles, DMMA).  Output row-major n_i x n_b per leaf.
+// ===========================================================================
+__device__ void block_uinv(const Grp& G, const double* M, const short* perm, int ld, int r0, int w,
+                           double* Us, double* uinv) {
+  const int tid = G.tid, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < 64 * 64; e += NT) {
+    const int i = e >> 6, k = e & 63;
+    Us[i * 65 + k] = (i < w && k < w) ? (k >= i ? M[(size_t)perm[r0 + i] * ld + r0 + k] : 0.0)
+                                      : (i == k ? 1.0 : 0.0);
+  }
+  G.sync();
+  const int j = 8 * warp + (lane >> 2), q = lane & 3;
+  double x[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) x[r] = (4 * r + q == j) ? 1.0 : 0.0;
+#pragma unroll
+  for (int k = 63; k >= 0; --k) {
+    if (q == (k & 3)) x[k >> 2] = x[k >> 2] / Us[k * 65 + k];
+    const double xk = __shfl_sync(0xffffffffu, x[k >> 2], (lane & ~3) | (k & 3));
+#pragma unroll
+    for (int r = 0; r < 16; ++r)
+      if (4 * r + q < k) x[r] = fma(-Us[(4 * r + q) * 65 + k], xk, x[r]);
+  }
+#pragma unroll
+  for (int r = 0; r < 16; ++r) uinv[(4 * r + q) * 64 + j] = x[r];
+  __threadfence_block();
+  G.sync();
+}
+
+__global__ void __launch_bounds__(NT, 2) k3_ssolve_kernel(LuArgs a, double* __restrict__ S_out,
+                                                         double* __restrict__ uinv_ws, int n_leaves) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem* sm = reinterpret_cast<Smem*>(smem_raw);
+  const Grp G{(int)threadIdx.x, 0};
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(&sm->full[s], NT);
+      mbar_init(&sm->empty[s], NT / 32);
+    }
+    sm->gchunk = 0;
+  }
+  __syncthreads();
+  const LeafDims d = a.d;
+  const int ld = d.ld;
+  for (int leaf = blockIdx.x; leaf < n_leaves; leaf += gridDim.x) {
+    double* Mw = a.ws + (size_t)leaf * d.leaf_stride;
+    const double* M = Mw;
+    const short* perm_g = a.perm + (size_t)leaf * d.Rpad;
+    double* uinv = uinv_ws + (size_t)blockIdx.x * 4096;
+    for (int i = threadIdx.x; i < MAX_RPAD; i += NT) sm->perm[i] = i < d.Rpad ? perm_g[i] : (short)(d.Rpad - 1);
+    __syncthreads();
+    const short* perm = sm->perm;
+    const int ct_end = d.tb0 + d.nb;
+    for (int I = d.nblk - 1; I >= 0; --I) {
+      const int r0 = 64 * I, w = min(64, d.ni - r0);
+      block_uinv(G, M, perm, ld, r0, w, sm->pipe, uinv);
+      const int K = max(0, d.ni - r0 - 64);
+      for (int ct = d.tb0; ct < ct_end; ct += 128) {
+        auto crow = [=](int i) -> double* { return Mw + (size_t)perm[r0 + i] * ld + ct; };
+        auto arow = [=](int i) -> const double* { return M + (size_t)perm[r0 + i] * ld + r0 + 64; };
+        auto brow = [=](int k) -> const double* { return M + (size_t)perm[r0 + 64 + k] * ld + ct; };
+        Acc acc;
+        auto init = [&](Acc& x) { acc_load<TileU>(x, crow, 64); };
+        tile_mma<TileU>(G, acc, init, arow, brow, K, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
+        linv_apply(G, acc, uinv, sm->pipe);
+        acc_store<TileU>(acc, crow, w, min(128, ct_end - ct));
+      }
+      __threadfence_block();
+      __syncthreads();
+    }
+    double* Sl = S_out + (size_t)leaf * d.ni * d.nb;
+    for (int e = threadIdx.x; e < d.ni * d.nb; e += NT) {
+      const int k = e / d.nb, c = e % d.nb;
+      Sl[e] = -M[(size_t)perm[k] * ld + d.tb0 + c];
+    }
+    __syncthreads();
+  }
+}
+
+void launch_ssolve(const LuArgs& a, double* S_out, double* uinv_ws, int n_leaves, cudaStream_t st) {
+  if (n_leaves <= 0) return;
+  cudaFuncSetAttribute(k3_ssolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(Smem));
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = n_leaves < 2 * sms ? n_leaves : 2 * sms;
+  k3_ssolve_kernel<<<grid, NT, sizeof(Smem), st>>>(a, S_out, uinv_ws, n_leaves);
+}
+
 template <int NSLOT>
 static void launch_ns(const LuArgs& a, int n_leaves, cudaStream_t st) {
   int dev = 0, sms = 148;

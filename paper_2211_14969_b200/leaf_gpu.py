@@ -161,8 +161,9 @@ class LeafStage:
         self._check(lib().hps_gpu_set_fault_injection(self._h, _ptr(el), el.size))
 
     # -- batched_condense ---------------------------------------------------------------------
-    def condense(self, b, f, e0=0, out=None, raise_on_resonance=True):
-        """b, f: (n, p*p) host arrays for elements [e0, e0+n).  Returns (T, w, status)."""
+    def condense(self, b, f, e0=0, out=None, raise_on_resonance=True, want_S=False):
+        """b, f: (n, p*p) host arrays for elements [e0, e0+n).  Returns (T, w, status), plus
+        S_solve (n, n_i, n_b) when want_S."""
         pp = self.p * self.p
         b = _f64(b, (-1, pp)); f = _f64(f, (-1, pp))
         n = b.shape[0]
@@ -170,11 +171,12 @@ class LeafStage:
             T = np.empty((n, self.n_b, self.n_b)); w = np.empty((n, self.n_b))
         else:
             T, w = out
+        S = np.empty((n, self.n_i, self.n_b)) if want_S else None
         st = np.zeros(n, np.int32)
-        rc = lib().hps_gpu_condense(self._h, e0, e0 + n, _ptr(b), _ptr(f), _ptr(T), _ptr(w), None, _ptr(st))
+        rc = lib().hps_gpu_condense(self._h, e0, e0 + n, _ptr(b), _ptr(f), _ptr(T), _ptr(w), _ptr(S), _ptr(st))
         if rc != HPS_OK and (rc != HPS_ERR_RESONANCE or raise_on_resonance):
             self._check(rc, st, e0)
-        return T, w, st
+        return (T, w, st, S) if want_S else (T, w, st)
 
     def condense_device(self, e0, n, d_b, d_f, d_T, d_w, d_status, stream=0):
         """Device-resident variant: arguments are raw device pointers (ints)."""

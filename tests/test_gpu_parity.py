@@ -258,3 +258,20 @@ def test_fused_assembly_equals_materialised_k1(monkeypatch):
         T2, w2, _ = st.condense(b, f)
     assert np.array_equal(T1.view(np.int64), T2.view(np.int64))
     assert np.array_equal(w1.view(np.int64), w2.view(np.int64))
+
+
+@pytest.mark.parametrize("p,kappa,n", [(6, 5.0, 3), (12, 20.0, 4), (13, 9.0, 3), (22, 100.0, 3), (42, 500.0, 2)])
+def test_s_solve_parity(p, kappa, n):
+    """K3: S_solve = -A_ii^{-1} A_ib vs the oracle (dgetrs), relFro <= 1e-10,
+    and T = D_b + D_i S_solve holds for the GPU's own S."""
+    b, f = random_leaves(p, n, seed=200 + p)
+    a = 1.0 / n
+    ref = O.batched_condense(p, a, kappa, b, f, want_S=True)
+    with G().LeafStage(p, n, 1, kappa, a=a) as st:
+        T, w, s, S = st.condense(b, f, want_S=True)
+    assert rel_fro(S, ref["S"]).max() <= TOL_T
+    it, bd = O.leaf_index(p)
+    for e in range(n):
+        _, Dn = O.build_leaf(p, a, kappa, b[e])
+        Tchk = Dn[:, bd] + Dn[:, it] @ S[e]
+        assert np.linalg.norm(Tchk - T[e]) <= 1e-10 * np.linalg.norm(T[e])

@@ -359,7 +359,8 @@ __device__ __forceinline__ unsigned long long pivot_key(double v, int phys) {
 }
 
 template <int NSLOT>
-__device__ void base_strip(const Grp& G, const LeafCtx& L, int e, int sw, double& minpiv) {
+__device__ void base_strip(const Grp& G, const LeafCtx& L, int e, int sw, double& minpiv,
+                           const double* sbuf) {
   const int tid = G.tid, lane = tid & 31, warp = tid >> 5;
   const int nrows = L.R - e;
   double x[NSLOT][4];
@@ -373,10 +374,16 @@ __device__ void base_strip(const Grp& G, const LeafCtx& L, int e, int sw, double
     if (idx < nrows) {
       phys[s] = L.perm[e + idx];
       active |= 1u << s;
-      const double* src = L.M + (size_t)phys[s] * L.ld + e;
+      if (sbuf) {   // handed over in shared memory by the preceding panel_update
+        const double2 v0 = *reinterpret_cast<const double2*>(sbuf + 4 * idx);
+        const double2 v1 = *reinterpret_cast<const double2*>(sbuf + 4 * idx + 2);
+        x[s][0] = v0.x; x[s][1] = v0.y; x[s][2] = v1.x; x[s][3] = v1.y;
+      } else {
+        const double* src = L.M + (size_t)phys[s] * L.ld + e;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (j < sw) x[s][j] = src[j];
+        for (int j = 0; j < 4; ++j)
+          if (j < sw) x[s][j] = src[j];
+      }
     }
   }
   G.sync();  // all perm reads done before thread 0 starts swapping
@@ -466,7 +473,7 @@ constexpr int XS = 36;  // stride of the in-panel h x nd blocks (== 4 mod 16: co
 //   L part (rows d0..R-1)   :  C -= A[:, src] X    DMMA m8n8k4, one 8-row group per warp
 template <int H>
 __device__ void panel_update_t(const Grp& G, const LeafCtx& L, int s0, int d0, int nd, long long* pc,
-                               long long& t_phase) {
+                               long long& t_phase, double* sbuf) {
   constexpr int NTILE = (H + 7) / 8;        // 8-wide DMMA column tiles (nd <= H)
   constexpr int UNR = H <= 8 ? 4 : 2;       // 8-row groups in flight per warp
   constexpr int KS = H / 4;                 // DMMA k-steps
@@ -541,6 +548,11 @@ __device__ void panel_update_t(const Grp& G, const LeafCtx& L, int s0, int d0, i
           row[u][d0 + c] = acc[u][ni][0];
         }
       }
+      // the next base strip (columns d0..d0+3, rows d0..R-1) reads these from shared memory
+      if (t < 2) {
+        const int r = base + 8 * (NT / 32) * u + g;
+        *reinterpret_cast<double2*>(sbuf + 4 * (r - d0) + 2 * t) = make_double2(acc[u][0][0], acc[u][0][1]);
+      }
     }
   }
   __threadfence_block();
@@ -553,12 +565,12 @@ __device__ void panel_update_t(const Grp& G, const LeafCtx& L, int s0, int d0, i
 //   U part (rows s0..s0+h-1):  X = L_hh^{-1} X     one warp, column per lane, registers
 //   L part (rows d0..R-1)   :  C -= A[:, src] X    DMMA m8n8k4 over 8-row groups
 __device__ void panel_update(const Grp& G, const LeafCtx& L, int s0, int h, int d0, int nd,
-                             long long* pc, long long& t_phase) {
+                             long long* pc, long long& t_phase, double* sbuf) {
   switch (h) {
-    case 4: panel_update_t<4>(G, L, s0, d0, nd, pc, t_phase); break;
-    case 8: panel_update_t<8>(G, L, s0, d0, nd, pc, t_phase); break;
-    case 16: panel_update_t<16>(G, L, s0, d0, nd, pc, t_phase); break;
-    default: panel_update_t<32>(G, L, s0, d0, nd, pc, t_phase); break;
+    case 4: panel_update_t<4>(G, L, s0, d0, nd, pc, t_phase, sbuf); break;
+    case 8: panel_update_t<8>(G, L, s0, d0, nd, pc, t_phase, sbuf); break;
+    case 16: panel_update_t<16>(G, L, s0, d0, nd, pc, t_phase, sbuf); break;
+    default: panel_update_t<32>(G, L, s0, d0, nd, pc, t_phase, sbuf); break;
   }
 }
 
@@ -595,15 +607,19 @@ __device__ void panel_linv(const Grp& G, const LeafCtx& L, int c0, int w, double
 template <int NSLOT>
 __device__ void panel_factor(const Grp& G, const LeafCtx& L, int c0, int w, double& minpiv,
                              long long* pc, long long& t_phase) {
+  double* sbuf = L.scratch + 2 * 32 * XS;   // R x 4 strip hand-off (after the update's Ls/X)
+  bool handed = false;
   for (int e = c0; e < c0 + w;) {
     const int sw = min(4, c0 + w - e);
-    base_strip<NSLOT>(G, L, e, sw, minpiv);
+    base_strip<NSLOT>(G, L, e, sw, minpiv, handed ? sbuf : nullptr);
     PHASE_MARK(5);
     e += sw;
     const int done = e - c0;
+    handed = false;
     if (done < w) {
       const int h = done & (-done);      // lowest set bit: recursive-LU schedule
-      panel_update(G, L, e - h, h, e, min(h, c0 + w - e), pc, t_phase);
+      panel_update(G, L, e - h, h, e, min(h, c0 + w - e), pc, t_phase, sbuf);
+      handed = true;
     }
   }
 }
@@ -796,7 +812,7 @@ __global__ void __launch_bounds__(NT, 2) k2_lu_schur_kernel(LuArgs a, int n_leav
 // split of K between the partial and the remainder pass differs for the L part.
 // ===========================================================================
 constexpr int NT_LA = 2 * NT;
-constexpr int PAN_DBL = 64 * 65;
+constexpr int PAN_DBL = 2 * 32 * 36 + 4 * 2048;   // update Ls/X + strip hand-off (>= 64*65 for Linv)
 constexpr int PIPE_LA = cmax(cmax(TileL2::NS * TileL2::STAGE, TileU2::NS * TileU2::STAGE), 64 * LS_U);
 
 struct SmemLA {

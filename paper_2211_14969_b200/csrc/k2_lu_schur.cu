@@ -189,8 +189,9 @@ __device__ void tile_mma(const Grp& G, Acc& acc, const Init& init, const ARow& a
   for (int s = 0; s < NS_ - 1; ++s)
     if (s < nch) fill(s);
   init(acc);   // C-init (load or first-touch assembly) overlaps the prologue copies
+  // The refill of the stage freed by chunk c-1 is issued while computing chunk c (before its
+  // last k-step): the wait for the slowest warp to release that stage is then mostly hidden.
   for (int c = 0; c < nch; ++c) {
-    if (c + NS_ - 1 < nch) fill(c + NS_ - 1);
     const unsigned gc = g0 + c;
     const int st = gc % NS_;
     mbar_wait(&full[st], (gc / NS_) & 1u);
@@ -198,6 +199,7 @@ __device__ void tile_mma(const Grp& G, Acc& acc, const Init& init, const ARow& a
     const double* Bs = As + (TL::WM * 32) * TL::LDA;
 #pragma unroll
     for (int kk = 0; kk < KC_ / 4; ++kk) {
+      if (kk == KC_ / 4 - 1 && c + NS_ - 1 < nch) fill(c + NS_ - 1);
       double a[4], b[4];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi) a[mi] = sign * As[(32 * wm + 8 * mi + g) * TL::LDA + 4 * kk + t];

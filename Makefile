@@ -8,16 +8,28 @@ NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-ffp-contract=off
 SRC       := paper_2211_14969_b200/csrc
 OBJDIR    := build/obj
 LIB       := paper_2211_14969_b200/_lib/libhps_leaf_b200.so
-CU        := $(SRC)/k1_assemble.cu $(SRC)/k2_lu_schur.cu $(SRC)/k4_scatter.cu $(SRC)/k5_leaf_solve.cu
+CU        := $(SRC)/k1_assemble.cu $(SRC)/k4_scatter.cu $(SRC)/k5_leaf_solve.cu
 CPP       := $(SRC)/hps_host.cpp $(SRC)/hps_api.cpp
 HDRS      := $(wildcard $(SRC)/*.h $(SRC)/*.cuh include/*.h include/hps/*.hpp)
-OBJS      := $(patsubst $(SRC)/%,$(OBJDIR)/%.o,$(CU) $(CPP))
+# K2/K3 are built twice: 8-warp CTAs (g256) and 4-warp CTAs for small leaves (g128).
+K2OBJS    := $(OBJDIR)/k2_g256.o $(OBJDIR)/k2_g128.o
+OBJS      := $(patsubst $(SRC)/%,$(OBJDIR)/%.o,$(CU) $(CPP)) $(K2OBJS)
 
 all: $(LIB) oracle
 
 $(OBJDIR)/%.cu.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ > $(OBJDIR)/$*.ptxas.log 2>&1 || (cat $(OBJDIR)/$*.ptxas.log; exit 1)
+
+$(OBJDIR)/k2_g256.o: $(SRC)/k2_lu_schur.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -DHPS_NT=256 -DHPS_CFG=g256 -DHPS_CTAS=2 -DHPS_NSTAGE=3 -DHPS_MAX_ROWS=2048 \
+	    -c $< -o $@ > $(OBJDIR)/k2_g256.ptxas.log 2>&1 || (cat $(OBJDIR)/k2_g256.ptxas.log; exit 1)
+
+$(OBJDIR)/k2_g128.o: $(SRC)/k2_lu_schur.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -DHPS_NT=128 -DHPS_CFG=g128 -DHPS_CTAS=4 -DHPS_NSTAGE=2 -DHPS_MAX_ROWS=640 \
+	    -c $< -o $@ > $(OBJDIR)/k2_g128.ptxas.log 2>&1 || (cat $(OBJDIR)/k2_g128.ptxas.log; exit 1)
 
 $(OBJDIR)/%.cpp.o: $(SRC)/%.cpp $(HDRS)
 	@mkdir -p $(OBJDIR)

@@ -215,6 +215,8 @@ struct hps_gpu_ctx {
   // kernel measured faster on C2/C3/C4 in round 1.
   bool lookahead = std::getenv("HPS_LOOKAHEAD") && std::getenv("HPS_LOOKAHEAD")[0] == '1';
   long long dephase_ns = std::getenv("HPS_DEPHASE_NS") ? std::atoll(std::getenv("HPS_DEPHASE_NS")) : 0;
+  // HPS_K2_CFG=128|256 forces the K2 build (default: by leaf size, hps_kernels.h use_g128).
+  int force_cfg = std::getenv("HPS_K2_CFG") ? std::atoi(std::getenv("HPS_K2_CFG")) : 0;
   DevBuf phase_buf;
   int store_e0 = -1, store_e1 = -1;
 
@@ -361,7 +363,7 @@ void enqueue_condense_chunk(hps_gpu_ctx* ctx, int e, int n, const double* d_b, c
     cudaMemsetAsync(ctx->phase_buf.ptr, 0, size_t(n) * 8 * sizeof(long long), st);
     a.phase_cycles = ctx->phase_buf.as<long long>();
   }
-  hpsg::launch_lu_schur(a, n, st);
+  hpsg::launch_lu_schur(a, n, st, ctx->force_cfg);
   cudaEventRecord(ctx->timing_event(3 * ci + 2), st);
   if (ctx->phase_timers) {
     std::vector<long long> h(size_t(n) * 8);
@@ -592,7 +594,7 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
     CK(ctx->out_st[i].ensure(size_t(chunk) * 4));
     if (S) CK(ctx->out_S[i].ensure(size_t(chunk) * d.ni * d.nb * 8));
   }
-  if (S) CK(ctx->uinv.ensure(size_t(2 * ctx->sms) * 4096 * 8));
+  if (S) CK(ctx->uinv.ensure(size_t(4 * ctx->sms) * 4096 * 8));
   const size_t nis = size_t(d.ni) * d.nb;
   reset_timing(ctx);
   int ci = 0;
@@ -614,7 +616,8 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
       a3.d = d;
       a3.ws = ctx->ws.as<double>();
       a3.perm = ctx->perm.as<short>();
-      hpsg::launch_ssolve(a3, ctx->out_S[k].as<double>(), ctx->uinv.as<double>(), n, ctx->s_comp);
+      hpsg::launch_ssolve(a3, ctx->out_S[k].as<double>(), ctx->uinv.as<double>(), n, ctx->s_comp,
+                          ctx->force_cfg);
       ctx->tkernels += 1;
     }
     CK(cudaGetLastError());

@@ -28,6 +28,7 @@ void launch_write_rhs(const LeafDims& d, int col, const double* D2, const double
                       const double* v, double* ws, int n_leaves, cudaStream_t st);
 
 // K2+K3: blocked LU + triangular solves + Schur GEMM -> T, w, status.
+struct LuArgs;
 struct LuArgs {
   LeafDims d;           // geometry; R = ni and ntb = 1 for leaf solves
   double* ws;           // leaf workspaces (leaf_stride apart)
@@ -54,11 +55,35 @@ struct LuArgs {
   const double* f = nullptr;           // p*p per leaf
   const int* inject = nullptr;         // per leaf, nullable
 };
-size_t lu_smem_bytes();
-// K3: S_solve = -A_ii^{-1} A_ib from a factored workspace (after K2).  uinv_ws: 4096
-// doubles per resident CTA (2 per SM).
-void launch_ssolve(const LuArgs& a, double* S_out, double* uinv_ws, int n_leaves, cudaStream_t st);
-void launch_lu_schur(const LuArgs& a, int n_leaves, cudaStream_t st);
+// Two builds of k2_lu_schur.cu: g256 (8-warp CTAs, R <= 2048) and g128 (4-warp CTAs,
+// R <= 640, more leaves per SM).  K3: S_solve = -A_ii^{-1} A_ib from a factored workspace
+// (after K2); uinv_ws holds 4096 doubles per resident CTA (<= 4 per SM).
+#define HPS_K2_DECL(ns)                                                                       \
+  namespace ns {                                                                              \
+  size_t lu_smem_bytes();                                                                     \
+  void launch_lu_schur(const LuArgs& a, int n_leaves, cudaStream_t st);                       \
+  void launch_ssolve(const LuArgs& a, double* S_out, double* uinv_ws, int n_leaves,           \
+                     cudaStream_t st);                                                        \
+  }
+HPS_K2_DECL(g256)
+HPS_K2_DECL(g128)
+#undef HPS_K2_DECL
+
+// Config choice: the 4-warp build for small leaves (R <= 640, p <= 24) unless forced.
+inline bool use_g128(const LeafDims& d, int force) {
+  if (force == 128) return d.R <= 640;
+  if (force == 256) return false;
+  return d.R <= 640;
+}
+inline void launch_lu_schur(const LuArgs& a, int n_leaves, cudaStream_t st, int force = 0) {
+  if (use_g128(a.d, force) && !a.lookahead) g128::launch_lu_schur(a, n_leaves, st);
+  else g256::launch_lu_schur(a, n_leaves, st);
+}
+inline void launch_ssolve(const LuArgs& a, double* S_out, double* uinv_ws, int n_leaves,
+                          cudaStream_t st, int force = 0) {
+  if (use_g128(a.d, force)) g128::launch_ssolve(a, S_out, uinv_ws, n_leaves, st);
+  else g256::launch_ssolve(a, S_out, uinv_ws, n_leaves, st);
+}
 
 // K5: back substitution u_i = U^{-1} y (y = L^{-1} P rhs in column tb0) and the
 // local solution vector u (p*p per leaf): interior from the solve, boundary = v.

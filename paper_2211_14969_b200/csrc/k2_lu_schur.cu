@@ -30,7 +30,19 @@
 #include "hps_device.cuh"
 #include "hps_kernels.h"
 
+#ifndef HPS_NT
+#define HPS_NT 256
+#endif
+#ifndef HPS_CFG
+#define HPS_CFG g256
+#endif
+
 namespace hpsg {
+// Two builds of this file (Makefile), each in its own namespace:
+//   g256: HPS_NT=256 (8-warp CTAs, 2 per SM, 3 stages, R <= 2048)  -- large p
+//   g128: HPS_NT=128 (4-warp CTAs, more leaves per SM, R <= 1024)   -- small p, where the
+//         latency-bound pivot panels dominate and more co-resident leaves hide them.
+namespace HPS_CFG {
 
 // Optional per-phase cycle counters (LuArgs::phase_cycles != nullptr): thread 0
 // accumulates clock64() deltas between CTA-wide barriers into 8 slots per leaf:
@@ -44,12 +56,23 @@ namespace hpsg {
     }                                                                        \
   } while (0)
 
-constexpr int NT = 256;              // threads per CTA (8 warps, 32x32 warp tiles)
-constexpr int KC = 16;               // K chunk per stage (2-leaves-per-SM kernel)
-constexpr int NSTAGE = 3;            // stages (2-leaves-per-SM kernel)
+constexpr int NT = HPS_NT;           // threads per CTA / group (32x32 warp tiles)
+constexpr int NWARP = NT / 32;
+#ifndef HPS_NSTAGE
+#define HPS_NSTAGE 3
+#endif
+#ifndef HPS_CTAS
+#define HPS_CTAS 2
+#endif
+#ifndef HPS_MAX_ROWS
+#define HPS_MAX_ROWS 2048
+#endif
+constexpr int KC = 16;               // K chunk per stage
+constexpr int NSTAGE = HPS_NSTAGE;   // pipeline stages
 constexpr int MAX_NSTAGE = 4;
-constexpr int MAX_NSLOT = 8;         // strip rows per thread: R <= 2048 (p <= 45)
-constexpr int MAX_RPAD = 2048 + 128; // perm entries (tile gathers may run 127 past R)
+constexpr int MAX_NSLOT = 8;
+static_assert(MAX_NSLOT * NT >= HPS_MAX_ROWS, "strip rows per thread");         // strip rows per thread: R <= 2048 (p <= 45)
+constexpr int MAX_RPAD = HPS_MAX_ROWS + 128;  // perm entries (tile gathers may run past R)
 
 // A group of 256 threads (8 warps) sharing a named barrier.  The one-leaf-per-CTA kernel
 // uses the whole CTA (barrier 0); the lookahead kernel runs a GEMM group (threads 0-255,
@@ -76,25 +99,38 @@ struct Tile {
   static constexpr int AGR = TM_ * KC_ / 2 / NT;      // 16-byte A granules / thread / chunk
   static constexpr int BGR = KC_ * TN_ / 2 / NT;      // 16-byte B granules / thread / chunk
   static constexpr int BROW = TN_ / 2;                // granules per B row
-  static_assert(WM * WN == NT / 32, "8 warps");
+  static_assert(WM * WN == NT / 32, "one 32x32 warp tile per warp");
   static_assert(NS_ <= MAX_NSTAGE, "stages");
 };
+#if HPS_NT == 256
 using TileL = Tile<128, 64>;
 using TileU = Tile<64, 128>;
+#else
+using TileL = Tile<64, 64>;
+using TileU = Tile<64, 64>;
+#endif
+constexpr int TLM = TileL::WM * 32;  // L-part / D-row tile rows
+constexpr int TUN = TileU::WN * 32;  // U-part tile columns
+#if HPS_NT == 256
 // Lookahead kernel (1 CTA/SM, more shared memory): 4 stages.
 using TileL2 = Tile<128, 64, 16, 4>;
 using TileU2 = Tile<64, 128, 16, 4>;
-constexpr int LS_U = 132;            // Linv-apply staging of a 64x128 U tile (== 4 mod 16)
+#endif
+constexpr int LS_U = TUN + 4;        // Linv-apply staging of a 64 x TUN U tile (== 4 mod 16)
 constexpr int cmax(int a, int b) { return a > b ? a : b; }
-constexpr int PIPE_DBL = cmax(cmax(NSTAGE * TileL::STAGE, NSTAGE * TileU::STAGE), 64 * LS_U);
+// The pipeline region doubles as panel scratch: in-panel update blocks (2 x 32 x 36),
+// the strip hand-off (4 x rows) and the Linv/Uinv staging (64 x 65).
+constexpr int PANEL_DBL = cmax(2 * 32 * 36 + 4 * HPS_MAX_ROWS, 64 * 65);
+constexpr int PIPE_DBL =
+    cmax(cmax(cmax(NSTAGE * TileL::STAGE, NSTAGE * TileU::STAGE), 64 * LS_U), PANEL_DBL);
 
 struct Smem {
   double pipe[PIPE_DBL];             // tile-job pipeline, re-used by the panel code
   unsigned long long full[NSTAGE];   // stage filled (256 thread arrivals)
   unsigned long long empty[NSTAGE];  // stage consumed (8 warp arrivals)
   unsigned gchunk;                   // running K-chunk counter of this CTA
-  double wrow[2][NT / 32][4];        // per-warp pivot candidate rows (double-buffered)
-  unsigned long long redk[2][NT / 32];
+  double wrow[2][NWARP][4];          // per-warp pivot candidate rows (double-buffered)
+  unsigned long long redk[2][NWARP];
   short perm[MAX_RPAD];              // logical -> physical row
   short iperm[MAX_RPAD];             // physical -> logical row
 };
@@ -408,30 +444,30 @@ __device__ void base_strip(const Grp& G, const LeafCtx& L, int e, int sw, double
       const unsigned long long ok = __shfl_xor_sync(0xffffffffu, wbest, o);
       wbest = ok > wbest ? ok : wbest;
     }
-    if (lane == 0) L.redk[buf * 8 + warp] = wbest;
+    if (lane == 0) L.redk[buf * NWARP + warp] = wbest;
     if (best == wbest && best != 0ull) {  // this lane owns the warp's candidate row
       double r0 = x[0][0], r1 = x[0][1], r2 = x[0][2], r3 = x[0][3];
 #pragma unroll
       for (int s = 1; s < NSLOT; ++s)
         if (s == bs) { r0 = x[s][0]; r1 = x[s][1]; r2 = x[s][2]; r3 = x[s][3]; }
-      double* wr = L.wrow + (buf * 8 + warp) * 4;
+      double* wr = L.wrow + (buf * NWARP + warp) * 4;
       wr[0] = r0;
       wr[1] = r1;
       wr[2] = r2;
       wr[3] = r3;
     }
     G.sync();
-    unsigned long long kb = L.redk[buf * 8];
+    unsigned long long kb = L.redk[buf * NWARP];
     int ww = 0;
 #pragma unroll
     for (int w = 1; w < NT / 32; ++w) {
-      const unsigned long long k = L.redk[buf * 8 + w];
+      const unsigned long long k = L.redk[buf * NWARP + w];
       if (k > kb) { kb = k; ww = w; }
     }
     const int pphys = 0x7FF - static_cast<int>(kb & 0x7FFull);
     double prow[4];
 #pragma unroll
-    for (int jj = 0; jj < 4; ++jj) prow[jj] = L.wrow[(buf * 8 + ww) * 4 + jj];
+    for (int jj = 0; jj < 4; ++jj) prow[jj] = L.wrow[(buf * NWARP + ww) * 4 + jj];
     const double piv = prow[j];
     const double rpiv = 1.0 / piv;   // dgetf2-style reciprocal scaling
     if (tid == 0) {
@@ -588,21 +624,23 @@ __device__ void panel_linv(const Grp& G, const LeafCtx& L, int c0, int w, double
     Ls[i * 65 + k] = (i < w && k < i) ? mrow(L, c0 + i)[c0 + k] : 0.0;
   }
   G.sync();
-  // lane (jj, q): column j = 8 warp + jj, rows i = 4 r + q (r < 16).  Rows interleaved by
+  // lane (jj, q): column j = jb + 8 warp + jj, rows i = 4 r + q (r < 16).  Rows interleaved by
   // quarter so the four quarters' Ls reads hit four different banks.
-  const int j = 8 * warp + (lane >> 2), q = lane & 3;
-  double x[16];
+  for (int jb = 0; jb < 64; jb += 8 * NWARP) {
+    const int j = jb + 8 * warp + (lane >> 2), q = lane & 3;
+    double x[16];
 #pragma unroll
-  for (int r = 0; r < 16; ++r) x[r] = (4 * r + q == j) ? 1.0 : 0.0;
+    for (int r = 0; r < 16; ++r) x[r] = (4 * r + q == j) ? 1.0 : 0.0;
 #pragma unroll
-  for (int k = 0; k < 63; ++k) {
-    const double xk = __shfl_sync(0xffffffffu, x[k >> 2], (lane & ~3) | (k & 3));
+    for (int k = 0; k < 63; ++k) {
+      const double xk = __shfl_sync(0xffffffffu, x[k >> 2], (lane & ~3) | (k & 3));
 #pragma unroll
-    for (int r = 0; r < 16; ++r)
-      if (4 * r + q > k) x[r] = fma(-Ls[(4 * r + q) * 65 + k], xk, x[r]);
+      for (int r = 0; r < 16; ++r)
+        if (4 * r + q > k) x[r] = fma(-Ls[(4 * r + q) * 65 + k], xk, x[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) linv[(4 * r + q) * 64 + j] = x[r];
   }
-#pragma unroll
-  for (int r = 0; r < 16; ++r) linv[(4 * r + q) * 64 + j] = x[r];
   G.sync();
 }
 
@@ -683,8 +721,8 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
     const int c0 = 64 * J;
     const int w = min(64, d.ni - c0);
     if (a.factor) {
-      for (int rt = c0; rt < d.R; rt += 128) {
-        const int nr = min(128, d.R - rt);
+      for (int rt = c0; rt < d.R; rt += TLM) {
+        const int nr = min(TLM, d.R - rt);
         auto crow = [=](int i) -> double* { return L.M + (size_t)perm[rt + i] * ld + c0; };
         Acc acc;
         auto init = [&](Acc& x) {
@@ -707,7 +745,7 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
     const double* li = Linv + (size_t)J * 4096;
     const int ct_begin = a.factor ? c0 + 64 : d.tb0;
     const int ct_end = d.tb0 + 64 * d.ntb;
-    for (int ct = ct_begin; ct < ct_end; ct += 128) {
+    for (int ct = ct_begin; ct < ct_end; ct += TUN) {
       auto crow = [=](int i) -> double* { return L.M + (size_t)perm[c0 + i] * ld + ct; };
       Acc acc;
       auto init = [&](Acc& x) {
@@ -718,7 +756,7 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
       auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + ct; };
       tile_mma<TileU>(G, acc, init, arow, brow, c0, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
       linv_apply(G, acc, li, sm->pipe);
-      acc_store<TileU>(acc, crow, w, min(128, ct_end - ct));
+      acc_store<TileU>(acc, crow, w, min(TUN, ct_end - ct));
     }
     __threadfence_block();
     G.sync();
@@ -731,8 +769,8 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
     const int c0 = d.tb0 + 64 * tb;
     double* Tl = a.T_out + (size_t)leaf * d.nb * d.nb;
     double* wl = a.w_out + (size_t)leaf * d.nb;
-    for (int rt = d.ni; rt < d.R; rt += 128) {
-      const int nr = min(128, d.R - rt);
+    for (int rt = d.ni; rt < d.R; rt += TLM) {
+      const int nr = min(TLM, d.R - rt);
       auto crow = [=](int i) -> double* { return L.M + (size_t)perm[rt + i] * ld + c0; };
       Acc acc;
       auto init = [&](Acc& x) {
@@ -780,8 +818,10 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
 // The second CTA of every SM (blockIdx >= gridDim/2; classic placement puts b and
 // b + #SM on one SM) starts `dephase_ns` late so the two co-resident leaves are not in
 // their (latency-bound) panel phases at the same time.
+constexpr int CTAS_PER_SM = HPS_CTAS;
+
 template <int NSLOT>
-__global__ void __launch_bounds__(NT, 2) k2_lu_schur_kernel(LuArgs a, int n_leaves) {
+__global__ void __launch_bounds__(NT, CTAS_PER_SM) k2_lu_schur_kernel(LuArgs a, int n_leaves) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem* sm = reinterpret_cast<Smem*>(smem_raw);
   if (threadIdx.x == 0) {
@@ -799,6 +839,7 @@ __global__ void __launch_bounds__(NT, 2) k2_lu_schur_kernel(LuArgs a, int n_leav
   for (int leaf = blockIdx.x; leaf < n_leaves; leaf += gridDim.x) process_leaf<NSLOT>(a, sm, leaf);
 }
 
+#if HPS_NT == 256
 // ===========================================================================
 // Lookahead kernel: one CTA (16 warps) per SM and leaf.  Warps 0-7 (GEMM group) run all
 // tile jobs; warps 8-15 (panel group) factor panel J while the GEMM group works on what
@@ -1028,6 +1069,8 @@ __global__ void __launch_bounds__(NT_LA, 1) k2_lu_lookahead_kernel(LuArgs a, int
   }
 }
 
+#endif  // HPS_NT == 256
+
 size_t lu_smem_bytes() { return sizeof(Smem); }
 
 // ===========================================================================
@@ -1047,25 +1090,27 @@ __device__ void block_uinv(const Grp& G, const double* M, const short* perm, int
                                       : (i == k ? 1.0 : 0.0);
   }
   G.sync();
-  const int j = 8 * warp + (lane >> 2), q = lane & 3;
-  double x[16];
+  for (int jb = 0; jb < 64; jb += 8 * NWARP) {
+    const int j = jb + 8 * warp + (lane >> 2), q = lane & 3;
+    double x[16];
 #pragma unroll
-  for (int r = 0; r < 16; ++r) x[r] = (4 * r + q == j) ? 1.0 : 0.0;
+    for (int r = 0; r < 16; ++r) x[r] = (4 * r + q == j) ? 1.0 : 0.0;
 #pragma unroll
-  for (int k = 63; k >= 0; --k) {
-    if (q == (k & 3)) x[k >> 2] = x[k >> 2] / Us[k * 65 + k];
-    const double xk = __shfl_sync(0xffffffffu, x[k >> 2], (lane & ~3) | (k & 3));
+    for (int k = 63; k >= 0; --k) {
+      if (q == (k & 3)) x[k >> 2] = x[k >> 2] / Us[k * 65 + k];
+      const double xk = __shfl_sync(0xffffffffu, x[k >> 2], (lane & ~3) | (k & 3));
 #pragma unroll
-    for (int r = 0; r < 16; ++r)
-      if (4 * r + q < k) x[r] = fma(-Us[(4 * r + q) * 65 + k], xk, x[r]);
+      for (int r = 0; r < 16; ++r)
+        if (4 * r + q < k) x[r] = fma(-Us[(4 * r + q) * 65 + k], xk, x[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < 16; ++r) uinv[(4 * r + q) * 64 + j] = x[r];
   }
-#pragma unroll
-  for (int r = 0; r < 16; ++r) uinv[(4 * r + q) * 64 + j] = x[r];
   __threadfence_block();
   G.sync();
 }
 
-__global__ void __launch_bounds__(NT, 2) k3_ssolve_kernel(LuArgs a, double* __restrict__ S_out,
+__global__ void __launch_bounds__(NT, CTAS_PER_SM) k3_ssolve_kernel(LuArgs a, double* __restrict__ S_out,
                                                          double* __restrict__ uinv_ws, int n_leaves) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem* sm = reinterpret_cast<Smem*>(smem_raw);
@@ -1093,7 +1138,7 @@ __global__ void __launch_bounds__(NT, 2) k3_ssolve_kernel(LuArgs a, double* __re
       const int r0 = 64 * I, w = min(64, d.ni - r0);
       block_uinv(G, M, perm, ld, r0, w, sm->pipe, uinv);
       const int K = max(0, d.ni - r0 - 64);
-      for (int ct = d.tb0; ct < ct_end; ct += 128) {
+      for (int ct = d.tb0; ct < ct_end; ct += TUN) {
         auto crow = [=](int i) -> double* { return Mw + (size_t)perm[r0 + i] * ld + ct; };
         auto arow = [=](int i) -> const double* { return M + (size_t)perm[r0 + i] * ld + r0 + 64; };
         auto brow = [=](int k) -> const double* { return M + (size_t)perm[r0 + 64 + k] * ld + ct; };
@@ -1101,7 +1146,7 @@ __global__ void __launch_bounds__(NT, 2) k3_ssolve_kernel(LuArgs a, double* __re
         auto init = [&](Acc& x) { acc_load<TileU>(x, crow, 64); };
         tile_mma<TileU>(G, acc, init, arow, brow, K, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
         linv_apply(G, acc, uinv, sm->pipe);
-        acc_store<TileU>(acc, crow, w, min(128, ct_end - ct));
+        acc_store<TileU>(acc, crow, w, min(TUN, ct_end - ct));
       }
       __threadfence_block();
       __syncthreads();
@@ -1121,7 +1166,7 @@ void launch_ssolve(const LuArgs& a, double* S_out, double* uinv_ws, int n_leaves
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int grid = n_leaves < 2 * sms ? n_leaves : 2 * sms;
+  const int grid = n_leaves < CTAS_PER_SM * sms ? n_leaves : CTAS_PER_SM * sms;
   k3_ssolve_kernel<<<grid, NT, sizeof(Smem), st>>>(a, S_out, uinv_ws, n_leaves);
 }
 
@@ -1130,6 +1175,7 @@ static void launch_ns(const LuArgs& a, int n_leaves, cudaStream_t st) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+#if HPS_NT == 256
   if (a.lookahead && a.factor && a.d.nb > 0) {
     cudaFuncSetAttribute(k2_lu_lookahead_kernel<NSLOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(SmemLA));
@@ -1137,13 +1183,14 @@ static void launch_ns(const LuArgs& a, int n_leaves, cudaStream_t st) {
     k2_lu_lookahead_kernel<NSLOT><<<grid, NT_LA, sizeof(SmemLA), st>>>(a, n_leaves);
     return;
   }
+#endif
   cudaFuncSetAttribute(k2_lu_schur_kernel<NSLOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(Smem));
-  const int grid = n_leaves < 2 * sms ? n_leaves : 2 * sms;
+  const int grid = n_leaves < CTAS_PER_SM * sms ? n_leaves : CTAS_PER_SM * sms;
   k2_lu_schur_kernel<NSLOT><<<grid, NT, sizeof(Smem), st>>>(a, n_leaves);
 }
 
-// Strip rows per thread = ceil(R / 256): register-resident pivot strips sized to p.
+// Strip rows per thread = ceil(R / NT): register-resident pivot strips sized to p.
 void launch_lu_schur(const LuArgs& a, int n_leaves, cudaStream_t st) {
   if (n_leaves <= 0) return;
   const int need = (a.d.R + NT - 1) / NT;
@@ -1152,4 +1199,5 @@ void launch_lu_schur(const LuArgs& a, int n_leaves, cudaStream_t st) {
   else launch_ns<8>(a, n_leaves, st);
 }
 
+}  // namespace HPS_CFG
 }  // namespace hpsg

@@ -32,10 +32,11 @@ __device__ __forceinline__ int node_col(int y, int x, int p, int tb0) {
   return tb0 + boundary_pos(y, x, p);
 }
 
-// K1: one CTA per kRows rows of one leaf.  Phase 1 streams zeros over the rows with
-// 16-byte stores (the operator is >95% zeros: HBM-write bound); phase 2 (after the
-// barrier) writes the <= 2(p-2)+5 structural nonzeros of each row -- one warp per row --
-// with exactly the entries a_entry / dn_entry evaluate (same IEEE sequence as the oracle).
+// K1: one CTA per kRows rows of one leaf, one warp per row.  Each warp first evaluates
+// its row's <= 2p+1 structural nonzeros into registers (table loads in flight), then all
+// threads stream zeros over the CTA's rows with 16-byte stores (the operator is >95%
+// zeros: HBM-write bound), and after the barrier the warps scatter their nonzeros --
+// exactly the entries a_entry / dn_entry evaluate (same IEEE sequence as the oracle).
 __global__ void __launch_bounds__(256) k1_assemble_kernel(
     LeafDims d, const int* __restrict__ rowcode, const int* __restrict__ colcode,
     const double* __restrict__ Ds, const double* __restrict__ D2, double k2,
@@ -50,56 +51,76 @@ __global__ void __launch_bounds__(256) k1_assemble_kernel(
   double* W = ws + (size_t)leaf * d.leaf_stride;
   const int half = d.ld >> 1;
   const int nrows = min(kRows, d.Rpad - r0);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = r0 + warp;
+  // ---- phase 0: this warp's row nonzeros into registers (2 line positions per lane) ----
+  double val[2][2];
+  int col[2][2];   // -1: nothing to write
+  double fval = 0.0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) col[h][0] = col[h][1] = -1;
+  if (warp < nrows && r < d.R) {
+    const int rc = __ldg(rowcode + r);
+    const int iy = rc & 255, ix = (rc >> 8) & 255;
+    if (r < d.ni) {
+      const int l = iy * p + ix;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = lane + 32 * h;
+        if (j >= p) continue;
+        // row line (jy == iy): node (iy, j)
+        const bool int_row = j >= 1 && j <= q;
+        if (!(int_row && inj && r == 0)) {
+          double v;
+          if (j == ix) {
+            v = -__ldg(D2 + iy * p + iy);
+            v = __dsub_rn(v, __ldg(D2 + ix * p + ix));
+            v = __dsub_rn(v, __dmul_rn(k2, __ldg(bl + l)));
+          } else {
+            v = -__ldg(D2 + ix * p + j);
+          }
+          val[h][0] = v;
+          col[h][0] = node_col(iy, j, p, d.tb0);
+        }
+        // column line (jx == ix, jy != iy): node (j, ix)
+        const bool int_col = j >= 1 && j <= q;
+        if (j != iy && !(int_col && inj && r == 0)) {
+          val[h][1] = -__ldg(D2 + iy * p + j);
+          col[h][1] = node_col(j, ix, p, d.tb0);
+        }
+      }
+      if (lane == 0) fval = __ldg(fl + l);
+    } else {
+      const int edge = (rc >> 18) & 3;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int j = lane + 32 * h;
+        if (j >= p) continue;
+        if (edge == 0 || edge == 2) {   // S: -d/dy, N: +d/dy along the column line
+          const double v = __ldg(Ds + iy * p + j);
+          val[h][0] = edge == 0 ? -v : v;
+          col[h][0] = node_col(j, ix, p, d.tb0);
+        } else {                        // E: +d/dx, W: -d/dx along the row line
+          const double v = __ldg(Ds + ix * p + j);
+          val[h][0] = edge == 3 ? -v : v;
+          col[h][0] = node_col(iy, j, p, d.tb0);
+        }
+      }
+    }
+  }
+  // ---- phase 1: stream zeros over the CTA's rows ----
   double2* W2 = reinterpret_cast<double2*>(W + (size_t)r0 * d.ld);
   for (int idx = threadIdx.x; idx < nrows * half; idx += blockDim.x) W2[idx] = make_double2(0.0, 0.0);
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = r0 + warp;
+  // ---- phase 2: scatter the nonzeros ----
   if (warp >= nrows || r >= d.R) return;
   double* row = W + (size_t)r * d.ld;
-  const int rc = __ldg(rowcode + r);
-  const int iy = rc & 255, ix = (rc >> 8) & 255;
-  if (r < d.ni) {
-    const int l = iy * p + ix;
-    // row line (jy == iy): interior columns jx = 1..q and the two boundary nodes (iy,0),(iy,p-1)
-    for (int jx = lane; jx < p; jx += 32) {
-      const bool interior = jx >= 1 && jx <= q;
-      if (interior && inj && r == 0) continue;
-      double v;
-      if (jx == ix) {
-        v = -__ldg(D2 + iy * p + iy);
-        v = __dsub_rn(v, __ldg(D2 + ix * p + ix));
-        v = __dsub_rn(v, __dmul_rn(k2, __ldg(bl + l)));
-      } else {
-        v = -__ldg(D2 + ix * p + jx);
-      }
-      row[node_col(iy, jx, p, d.tb0)] = v;
-    }
-    // column line (jx == ix, jy != iy): interior jy = 1..q and (0,ix), (p-1,ix)
-    for (int jy = lane; jy < p; jy += 32) {
-      if (jy == iy) continue;
-      const bool interior = jy >= 1 && jy <= q;
-      if (interior && inj && r == 0) continue;
-      row[node_col(jy, ix, p, d.tb0)] = -__ldg(D2 + iy * p + jy);
-    }
-    if (lane == 0) row[d.tb0 + d.nb] = __ldg(fl + l);
-  } else {
-    const int edge = (rc >> 18) & 3;
-    for (int j = lane; j < p; j += 32) {
-      int y, x;
-      double v;
-      if (edge == 0 || edge == 2) {   // S: -d/dy, N: +d/dy along the column line
-        y = j; x = ix;
-        v = __ldg(Ds + iy * p + j);
-        if (edge == 0) v = -v;
-      } else {                        // E: +d/dx, W: -d/dx along the row line
-        y = iy; x = j;
-        v = __ldg(Ds + ix * p + j);
-        if (edge == 3) v = -v;
-      }
-      row[node_col(y, x, p, d.tb0)] = v;
-    }
-  }
+#pragma unroll
+  for (int h = 0; h < 2; ++h)
+#pragma unroll
+    for (int t = 0; t < 2; ++t)
+      if (col[h][t] >= 0) row[col[h][t]] = val[h][t];
+  if (r < d.ni && lane == 0) row[d.tb0 + d.nb] = fval;
 }
 
 // ||A_ii||_inf per leaf: row sums over the sparse cross stencil in

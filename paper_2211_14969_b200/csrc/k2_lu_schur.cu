@@ -198,7 +198,8 @@ __device__ __forceinline__ void load_chunk(double* st, unsigned long long* full,
 template <class TL, class ARow, class BRow, class Init>
 __device__ void tile_mma(const Grp& G, Acc& acc, const Init& init, const ARow& arow, const BRow& brow,
                          int K, double sign, double* pipe, unsigned long long* full,
-                         unsigned long long* empty, unsigned* gchunk) {
+                         unsigned long long* empty, unsigned* gchunk, int mact = TL::WM * 32,
+                         int nact = TL::WN * 32) {
   constexpr int KC_ = TL::K, NS_ = TL::NS;
   const int nch = (K + KC_ - 1) / KC_;
   if (nch == 0) {
@@ -208,6 +209,9 @@ __device__ void tile_mma(const Grp& G, Acc& acc, const Init& init, const ARow& a
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp % TL::WM, wn = warp / TL::WM;
+  // Warps whose 32x32 tile lies wholly in the padding of a remainder tile (fewer than
+  // mact rows / nact columns are real) only stage operands: no DMMA on padding.
+  const bool act = 32 * wm < mact && 32 * wn < nact;
   const unsigned g0 = *gchunk;
   const double* pa[TL::AGR];
 #pragma unroll
@@ -233,6 +237,9 @@ __device__ void tile_mma(const Grp& G, Acc& acc, const Init& init, const ARow& a
     mbar_wait(&full[st], (gc / NS_) & 1u);
     const double* As = pipe + st * TL::STAGE;
     const double* Bs = As + (TL::WM * 32) * TL::LDA;
+    if (!act) {
+      if (c + NS_ - 1 < nch) fill(c + NS_ - 1);
+    } else
 #pragma unroll
     for (int kk = 0; kk < KC_ / 4; ++kk) {
       if (kk == KC_ / 4 - 1 && c + NS_ - 1 < nch) fill(c + NS_ - 1);
@@ -338,8 +345,12 @@ __device__ __forceinline__ void acc_store(const Acc& acc, const CRow& crow, int 
 // shared memory; Linv fragments come straight from global (32 KB per block row, L1/L2
 // resident across the block row's tiles).
 __device__ __forceinline__ void linv_apply(const Grp& G, Acc& acc, const double* __restrict__ linv,
-                                           double* pipe) {
+                                           double* pipe, int nact = TUN) {
   double* Cs = pipe;   // 64 x LS_U
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int wm = warp % TileU::WM, wn = warp / TileU::WM;
+  const bool act = 32 * wn < nact;   // each warp reads only its own 32 columns of Cs
+  if (act)
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -347,8 +358,7 @@ __device__ __forceinline__ void linv_apply(const Grp& G, Acc& acc, const double*
       *reinterpret_cast<double2*>(Cs + acc_row<TileU>(mi) * LS_U + acc_col<TileU>(ni)) =
           make_double2(acc.v[mi][ni][0], acc.v[mi][ni][1]);
   G.sync();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int wm = warp % TileU::WM, wn = warp / TileU::WM;
+  if (act) {
   acc_zero(acc);
 #pragma unroll 4
   for (int kk = 0; kk < 16; ++kk) {
@@ -361,6 +371,7 @@ __device__ __forceinline__ void linv_apply(const Grp& G, Acc& acc, const double*
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) dmma(acc.v[mi][ni][0], acc.v[mi][ni][1], av[mi], bv[ni]);
+  }
   }
   G.sync();
 }
@@ -731,7 +742,8 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
         };
         auto arow = lrow(rt);
         auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + c0; };
-        tile_mma<TileL>(G, acc, init, arow, brow, c0, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
+        tile_mma<TileL>(G, acc, init, arow, brow, c0, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk,
+                        nr);
         acc_store<TileL>(acc, crow, nr, 64);
       }
       __threadfence_block();
@@ -754,8 +766,10 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
       };
       auto arow = lrow(c0);
       auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + ct; };
-      tile_mma<TileU>(G, acc, init, arow, brow, c0, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
-      linv_apply(G, acc, li, sm->pipe);
+      const int nc = min(TUN, ct_end - ct);
+      tile_mma<TileU>(G, acc, init, arow, brow, c0, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk,
+                      64, nc);
+      linv_apply(G, acc, li, sm->pipe, nc);
       acc_store<TileU>(acc, crow, w, min(TUN, ct_end - ct));
     }
     __threadfence_block();
@@ -779,7 +793,8 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
       };
       auto arow = lrow(rt);
       auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + c0; };
-      tile_mma<TileL>(G, acc, init, arow, brow, d.ni, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
+      tile_mma<TileL>(G, acc, init, arow, brow, d.ni, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk,
+                      nr);
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi) {
         const int r = acc_row<TileL>(mi);

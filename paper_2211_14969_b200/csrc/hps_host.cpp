@@ -191,6 +191,7 @@ struct hps_gpu_ctx {
   int sms = 148;
   int n_leaves = 0;
   int chunk = 0;
+  int k2_ctas = 2;               // co-resident K2 CTAs per SM (occupancy query at create)
   size_t per_leaf = 0;
   std::string err;
   double k2 = 0.0;
@@ -490,8 +491,10 @@ int hps_gpu_create(int device, const hps_leaf_desc* desc, hps_gpu_ctx** out) {
     budget = size_t(double(fr) * 0.7);
   }
   int chunk = int(std::min<size_t>(size_t(c->n_leaves), budget / c->per_leaf));
-  const int slots = 2 * c->sms;
-  if (chunk > slots) chunk = chunk / slots * slots;
+  c->k2_ctas = hpsg::lu_ctas_per_sm(d, c->force_cfg);
+  const int slots = c->k2_ctas * c->sms;
+  // Several chunks: make each a whole number of waves.  Everything resident: one chunk.
+  if (chunk < c->n_leaves && chunk > slots) chunk = chunk / slots * slots;
   if (D.storage == HPS_STORAGE_STORE && chunk < c->n_leaves)
     return reject(HPS_ERR_PARAM, "ParameterError: storage policy 'store' needs the factors of all " +
                                      std::to_string(c->n_leaves) +
@@ -536,7 +539,7 @@ int hps_gpu_get_info(const hps_gpu_ctx* ctx, hps_gpu_info_t* out) {
   out->n_b = ctx->d.nb;
   out->n_leaves = ctx->n_leaves;
   out->chunk_leaves = ctx->chunk;
-  out->resident_ctas = 2 * ctx->sms;
+  out->resident_ctas = ctx->k2_ctas * ctx->sms;
   out->workspace_bytes_per_leaf = int64_t(ctx->per_leaf);
   out->n_active = ctx->mesh.n_active;
   out->N = int64_t(ctx->desc.nx * (ctx->d.p - 1) + 1) * int64_t(ctx->desc.ny * (ctx->d.p - 1) + 1);

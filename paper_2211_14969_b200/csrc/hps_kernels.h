@@ -61,6 +61,7 @@ struct LuArgs {
 #define HPS_K2_DECL(ns)                                                                       \
   namespace ns {                                                                              \
   size_t lu_smem_bytes();                                                                     \
+  int lu_ctas_per_sm(const LeafDims& d);                                                      \
   void launch_lu_schur(const LuArgs& a, int n_leaves, cudaStream_t st);                       \
   void launch_ssolve(const LuArgs& a, double* S_out, double* uinv_ws, int n_leaves,           \
                      cudaStream_t st);                                                        \
@@ -78,6 +79,10 @@ inline bool use_g128(const LeafDims& d, int force) {
 inline void launch_lu_schur(const LuArgs& a, int n_leaves, cudaStream_t st, int force = 0) {
   if (use_g128(a.d, force) && !a.lookahead) g128::launch_lu_schur(a, n_leaves, st);
   else g256::launch_lu_schur(a, n_leaves, st);
+}
+// Co-resident K2 CTAs per SM for leaves of shape d (occupancy query, not an assumption).
+inline int lu_ctas_per_sm(const LeafDims& d, int force = 0) {
+  return use_g128(d, force) ? g128::lu_ctas_per_sm(d) : g256::lu_ctas_per_sm(d);
 }
 inline void launch_ssolve(const LuArgs& a, double* S_out, double* uinv_ws, int n_leaves,
                           cudaStream_t st, int force = 0) {

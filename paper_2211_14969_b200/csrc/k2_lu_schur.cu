@@ -1201,8 +1201,27 @@ static void launch_ns(const LuArgs& a, int n_leaves, cudaStream_t st) {
 #endif
   cudaFuncSetAttribute(k2_lu_schur_kernel<NSLOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(Smem));
-  const int grid = n_leaves < CTAS_PER_SM * sms ? n_leaves : CTAS_PER_SM * sms;
+  // Persistent grid = what is actually co-resident (a grid larger than that would leave
+  // whole CTAs, each owning several leaves, waiting for a second wave).
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_lu_schur_kernel<NSLOT>, NT, sizeof(Smem));
+  if (per_sm < 1) per_sm = 1;
+  const int grid = n_leaves < per_sm * sms ? n_leaves : per_sm * sms;
   k2_lu_schur_kernel<NSLOT><<<grid, NT, sizeof(Smem), st>>>(a, n_leaves);
+}
+
+template <int NSLOT>
+static int ctas_ns() {
+  cudaFuncSetAttribute(k2_lu_schur_kernel<NSLOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sizeof(Smem));
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_lu_schur_kernel<NSLOT>, NT, sizeof(Smem));
+  return per_sm < 1 ? 1 : per_sm;
+}
+
+int lu_ctas_per_sm(const LeafDims& d) {
+  const int need = (d.R + NT - 1) / NT;
+  return need <= 2 ? ctas_ns<2>() : need <= 4 ? ctas_ns<4>() : ctas_ns<8>();
 }
 
 // Strip rows per thread = ceil(R / NT): register-resident pivot strips sized to p.

@@ -20,6 +20,7 @@ T = torch.empty((n, nb, nb), dtype=torch.float64, device="cuda"); w = torch.empt
 s = torch.empty(n, dtype=torch.int32, device="cuda")
 st = G.LeafStage(p, cfg["nx"], cfg["ny"], cfg["kappa"], a=cfg["a"])
 strm = torch.cuda.Stream()
+print("resident K2 CTAs:", st.info()["resident_ctas"], flush=True)
 torch.cuda.synchronize()
 for r in range(a.reps):
     st.reset_timing()

@@ -13,6 +13,12 @@ CPP       := $(SRC)/hps_host.cpp $(SRC)/hps_api.cpp
 HDRS      := $(wildcard $(SRC)/*.h $(SRC)/*.cuh include/*.h include/hps/*.hpp)
 # K2/K3 are built twice: 8-warp CTAs (g256) and 4-warp CTAs for small leaves (g128).
 K2OBJS    := $(OBJDIR)/k2_g256.o $(OBJDIR)/k2_g128.o
+# K2 tuning knobs (CTAs/SM, cp.async pipeline stages, K chunk); `make variant` builds A/B copies.
+G256_NSTAGE ?= 3
+G256_KC     ?= 16
+G128_CTAS   ?= 4
+G128_NSTAGE ?= 2
+G128_KC     ?= 16
 OBJS      := $(patsubst $(SRC)/%,$(OBJDIR)/%.o,$(CU) $(CPP)) $(K2OBJS)
 
 all: $(LIB) oracle
@@ -23,12 +29,12 @@ $(OBJDIR)/%.cu.o: $(SRC)/%.cu $(HDRS)
 
 $(OBJDIR)/k2_g256.o: $(SRC)/k2_lu_schur.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
-	$(NVCC) $(NVFLAGS) -DHPS_NT=256 -DHPS_CFG=g256 -DHPS_CTAS=2 -DHPS_NSTAGE=3 -DHPS_MAX_ROWS=2048 \
+	$(NVCC) $(NVFLAGS) -DHPS_NT=256 -DHPS_CFG=g256 -DHPS_CTAS=2 -DHPS_NSTAGE=$(G256_NSTAGE) -DHPS_KC=$(G256_KC) -DHPS_MAX_ROWS=2048 \
 	    -c $< -o $@ > $(OBJDIR)/k2_g256.ptxas.log 2>&1 || (cat $(OBJDIR)/k2_g256.ptxas.log; exit 1)
 
 $(OBJDIR)/k2_g128.o: $(SRC)/k2_lu_schur.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
-	$(NVCC) $(NVFLAGS) -DHPS_NT=128 -DHPS_CFG=g128 -DHPS_CTAS=4 -DHPS_NSTAGE=2 -DHPS_MAX_ROWS=640 \
+	$(NVCC) $(NVFLAGS) -DHPS_NT=128 -DHPS_CFG=g128 -DHPS_CTAS=$(G128_CTAS) -DHPS_NSTAGE=$(G128_NSTAGE) -DHPS_KC=$(G128_KC) -DHPS_MAX_ROWS=640 \
 	    -c $< -o $@ > $(OBJDIR)/k2_g128.ptxas.log 2>&1 || (cat $(OBJDIR)/k2_g128.ptxas.log; exit 1)
 
 $(OBJDIR)/%.cpp.o: $(SRC)/%.cpp $(HDRS)
@@ -55,3 +61,8 @@ $(CXX_TEST): tests/cxx/test_leaf_api.cpp include/hps/leaf_gpu.hpp include/hps_le
 	@mkdir -p build
 	g++ -std=c++20 -O2 -Iinclude -o $@ $< -L$(dir $(LIB)) -lhps_leaf_b200 \
 	    -Wl,-rpath,'$$ORIGIN/../paper_2211_14969_b200/_lib'
+
+# A/B copy of the library with other K2 knobs, e.g.
+#   make variant NAME=g128s3 G128_CTAS=3 G128_NSTAGE=3   -> build/variants/g128s3.so
+variant:
+	$(MAKE) OBJDIR=build/var_$(NAME) LIB=build/variants/$(NAME).so build/variants/$(NAME).so

@@ -217,6 +217,7 @@ struct hps_gpu_ctx {
   bool lookahead = std::getenv("HPS_LOOKAHEAD") && std::getenv("HPS_LOOKAHEAD")[0] == '1';
   long long dephase_ns = std::getenv("HPS_DEPHASE_NS") ? std::atoll(std::getenv("HPS_DEPHASE_NS")) : 0;
   // HPS_K2_CFG=128|256 forces the K2 build (default: by leaf size, hps_kernels.h use_g128).
+  int max_ctas = std::getenv("HPS_K2_CTAS") ? std::atoi(std::getenv("HPS_K2_CTAS")) : 0;
   int force_cfg = std::getenv("HPS_K2_CFG") ? std::atoi(std::getenv("HPS_K2_CFG")) : 0;
   DevBuf phase_buf;
   int store_e0 = -1, store_e1 = -1;
@@ -349,6 +350,7 @@ void enqueue_condense_chunk(hps_gpu_ctx* ctx, int e, int n, const double* d_b, c
   a.minratio = ctx->minratio.as<double>();
   a.factor = 1;
   a.dephase_ns = ctx->dephase_ns;
+  a.max_ctas_per_sm = ctx->max_ctas;
   a.fused = ctx->fused ? 1 : 0;
   a.lookahead = (ctx->lookahead && !ctx->fused) ? 1 : 0;
   a.rowcode = ctx->rowcode.as<int>();

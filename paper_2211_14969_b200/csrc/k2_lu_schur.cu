@@ -67,7 +67,10 @@ constexpr int NWARP = NT / 32;
 #ifndef HPS_MAX_ROWS
 #define HPS_MAX_ROWS 2048
 #endif
-constexpr int KC = 16;               // K chunk per stage
+#ifndef HPS_KC
+#define HPS_KC 16
+#endif
+constexpr int KC = HPS_KC;           // K chunk per stage
 constexpr int NSTAGE = HPS_NSTAGE;   // pipeline stages
 constexpr int MAX_NSTAGE = 4;
 constexpr int MAX_NSLOT = 8;
@@ -402,8 +405,10 @@ __device__ __forceinline__ double* mrow(const LeafCtx& L, int logical) {
 // warp publishes its winner and that row's strip values (double-buffered slots), so the
 // pivot row needs no second broadcast round.  Interchanges are bookkeeping only: thread 0
 // swaps perm/iperm after the barrier; nobody else reads them inside the strip.
+// Integer-only (the sign bit is masked, no fabs): FP64 instructions here would queue
+// behind the co-resident CTA's DMMA on the shared FP64 pipe.
 __device__ __forceinline__ unsigned long long pivot_key(double v, int phys) {
-  return (static_cast<unsigned long long>(__double_as_longlong(fabs(v))) & ~0x7FFull) |
+  return (static_cast<unsigned long long>(__double_as_longlong(v)) & 0x7FFFFFFFFFFFF800ull) |
          static_cast<unsigned long long>(0x7FF - phys);
 }
 
@@ -1205,6 +1210,7 @@ static void launch_ns(const LuArgs& a, int n_leaves, cudaStream_t st) {
   // whole CTAs, each owning several leaves, waiting for a second wave).
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_lu_schur_kernel<NSLOT>, NT, sizeof(Smem));
+  if (a.max_ctas_per_sm > 0 && a.max_ctas_per_sm < per_sm) per_sm = a.max_ctas_per_sm;
   if (per_sm < 1) per_sm = 1;
   const int grid = n_leaves < per_sm * sms ? n_leaves : per_sm * sms;
   k2_lu_schur_kernel<NSLOT><<<grid, NT, sizeof(Smem), st>>>(a, n_leaves);

@@ -14,7 +14,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libhps_leaf_b200.so")
+# HPS_LIB_PATH: load an alternative build of the same library (kernel-variant A/B runs).
+LIB_PATH = os.environ.get("HPS_LIB_PATH") or os.path.join(_HERE, "_lib", "libhps_leaf_b200.so")
 
 HPS_OK, HPS_ERR_RESONANCE, HPS_ERR_PARAM, HPS_ERR_CUDA = 0, 1, 2, 3
 STORAGE_RECOMPUTE, STORAGE_STORE = 0, 1

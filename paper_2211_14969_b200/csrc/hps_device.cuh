@@ -84,6 +84,18 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 #endif
 // .L2::256B: every 16-byte request also pulls the rest of its 256-byte segment into L2,
 // so a row's next K chunk is an L2 hit and DRAM sees 256-byte bursts.
+// 256-bit global accesses (sm_100: LDG/STG.E.ENL2.256): one 32-byte row segment per thread.
+__device__ __forceinline__ void st_v4(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d)
+               : "memory");
+}
+__device__ __forceinline__ void ld_v4(const double* p, double& a, double& b, double& c, double& d) {
+  asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(a), "=d"(b), "=d"(c), "=d"(d)
+               : "l"(p)
+               : "memory");
+}
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global" HPS_L2_PREFETCH " [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));

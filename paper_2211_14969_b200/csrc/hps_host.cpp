@@ -362,19 +362,19 @@ void enqueue_condense_chunk(hps_gpu_ctx* ctx, int e, int n, const double* d_b, c
   a.f = d_f;
   a.inject = inj;
   if (ctx->phase_timers) {
-    ctx->phase_buf.ensure(size_t(ctx->chunk) * 8 * sizeof(long long));
-    cudaMemsetAsync(ctx->phase_buf.ptr, 0, size_t(n) * 8 * sizeof(long long), st);
+    ctx->phase_buf.ensure(size_t(ctx->chunk) * 16 * sizeof(long long));
+    cudaMemsetAsync(ctx->phase_buf.ptr, 0, size_t(n) * 16 * sizeof(long long), st);
     a.phase_cycles = ctx->phase_buf.as<long long>();
   }
   hpsg::launch_lu_schur(a, n, st, ctx->force_cfg);
   cudaEventRecord(ctx->timing_event(3 * ci + 2), st);
   if (ctx->phase_timers) {
-    std::vector<long long> h(size_t(n) * 8);
+    std::vector<long long> h(size_t(n) * 16);
     cudaMemcpyAsync(h.data(), ctx->phase_buf.ptr, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
-    double sum[8] = {0};
+    double sum[16] = {0};
     for (int i = 0; i < n; ++i)
-      for (int k = 0; k < 8; ++k) sum[k] += double(h[size_t(i) * 8 + k]);
+      for (int k = 0; k < 16; ++k) sum[k] += double(h[size_t(i) * 16 + k]);
     if (a.lookahead)
       std::fprintf(stderr,
                    "[hps LA cycles/leaf] GEMM: wait-done %.3g window %.3g post-panel %.3g D-rows %.3g | "
@@ -382,10 +382,12 @@ void enqueue_condense_chunk(hps_gpu_ctx* ctx, int e, int n, const double* d_b, c
                    sum[0] / n, sum[1] / n, sum[2] / n, sum[5] / n, sum[3] / n, sum[4] / n);
     else
     std::fprintf(stderr,
-                 "[hps phase cycles/leaf] U-part %.3g  L-part %.3g  panel %.3g (strips %.3g upd-U %.3g "
-                 "upd-L %.3g)  linv %.3g  trailing %.3g\n",
-                 sum[0] / n, sum[1] / n, sum[2] / n + sum[5] / n + sum[6] / n + sum[7] / n, sum[5] / n,
-                 sum[6] / n, sum[7] / n, sum[3] / n, sum[4] / n);
+                 "[hps phase cycles/leaf] U-part %.3g  L-part %.3g  panel %.3g (strips %.3g [start %.3g "
+                 "columns %.3g end %.3g] upd-U %.3g upd-L %.3g)  linv %.3g  trailing %.3g\n",
+                 sum[0] / n, sum[1] / n,
+                 (sum[2] + sum[8] + sum[9] + sum[10] + sum[6] + sum[7]) / n,
+                 (sum[8] + sum[9] + sum[10]) / n, sum[8] / n, sum[9] / n, sum[10] / n, sum[6] / n,
+                 sum[7] / n, sum[3] / n, sum[4] / n);
   }
 }
 

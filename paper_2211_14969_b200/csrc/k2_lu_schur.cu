@@ -414,7 +414,7 @@ __device__ __forceinline__ unsigned long long pivot_key(double v, int phys) {
 
 template <int NSLOT>
 __device__ void base_strip(const Grp& G, const LeafCtx& L, int e, int sw, double& minpiv,
-                           const double* sbuf) {
+                           const double* sbuf, long long* pc, long long& t_phase) {
   const int tid = G.tid, lane = tid & 31, warp = tid >> 5;
   const int nrows = L.R - e;
   double x[NSLOT][4];
@@ -434,13 +434,18 @@ __device__ void base_strip(const Grp& G, const LeafCtx& L, int e, int sw, double
         x[s][0] = v0.x; x[s][1] = v0.y; x[s][2] = v1.x; x[s][3] = v1.y;
       } else {
         const double* src = L.M + (size_t)phys[s] * L.ld + e;
+        if (sw == 4) {
+          ld_v4(src, x[s][0], x[s][1], x[s][2], x[s][3]);   // e % 4 == 0, ld % 64 == 0
+        } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (j < sw) x[s][j] = src[j];
+          for (int j = 0; j < 4; ++j)
+            if (j < sw) x[s][j] = src[j];
+        }
       }
     }
   }
   G.sync();  // all perm reads done before thread 0 starts swapping
+  PHASE_MARK(8);
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     if (j >= sw) break;
@@ -507,16 +512,20 @@ __device__ void base_strip(const Grp& G, const LeafCtx& L, int e, int sw, double
       }
     }
   }
+  PHASE_MARK(9);
 #pragma unroll
   for (int s = 0; s < NSLOT; ++s) {
     if (phys[s] == 0x7FFF) continue;
     double* dst = L.M + (size_t)phys[s] * L.ld + e;
+    if (sw == 4) {
+      st_v4(dst, x[s][0], x[s][1], x[s][2], x[s][3]);       // one 32-byte segment per row
+    } else {
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (j < sw) dst[j] = x[s][j];
+      for (int j = 0; j < 4; ++j)
+        if (j < sw) dst[j] = x[s][j];
+    }
   }
-  __threadfence_block();
-  G.sync();
+  G.sync();   // bar.sync orders the global stores for the CTA's readers
 }
 
 constexpr int XS = 36;  // stride of the in-panel h x nd blocks (== 4 mod 16: conflict-free B fragments)
@@ -667,8 +676,8 @@ __device__ void panel_factor(const Grp& G, const LeafCtx& L, int c0, int w, doub
   bool handed = false;
   for (int e = c0; e < c0 + w;) {
     const int sw = min(4, c0 + w - e);
-    base_strip<NSLOT>(G, L, e, sw, minpiv, handed ? sbuf : nullptr);
-    PHASE_MARK(5);
+    base_strip<NSLOT>(G, L, e, sw, minpiv, handed ? sbuf : nullptr, pc, t_phase);
+    PHASE_MARK(10);
     e += sw;
     const int done = e - c0;
     handed = false;
@@ -707,7 +716,7 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
   }
   G.sync();
   double minpiv = INFINITY;  // meaningful on thread 0
-  long long* pc = a.phase_cycles ? a.phase_cycles + (size_t)leaf * 8 : nullptr;
+  long long* pc = a.phase_cycles ? a.phase_cycles + (size_t)leaf * 16 : nullptr;
   Orig orig;
   orig.rowcode = a.rowcode;
   orig.colcode = a.colcode;
@@ -916,7 +925,7 @@ __device__ void process_leaf_la(const LuArgs& a, SmemLA* sm, const int leaf, con
   __syncthreads();
   // optional timers (thread 0 of each group): GEMM 0 wait-done 1 window 2 post-panel 5 D rows;
   // panel 3 wait-ready 4 factor+linv
-  long long* pcl = a.phase_cycles ? a.phase_cycles + (size_t)leaf * 8 : nullptr;
+  long long* pcl = a.phase_cycles ? a.phase_cycles + (size_t)leaf * 16 : nullptr;
   long long* pc = nullptr;      // (in-panel sub-phase marks off)
   long long t_phase = 0;
   long long tl = clock64();

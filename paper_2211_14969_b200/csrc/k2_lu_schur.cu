@@ -543,13 +543,31 @@ __device__ void panel_update_t(const Grp& G, const LeafCtx& L, int s0, int d0, i
   double* Ls = L.scratch;              // H x H   (stride XS)
   double* X = L.scratch + 32 * XS;     // H x 8*NTILE (stride XS), zero padded
   const int tid = G.tid, lane = tid & 31, warp = tid >> 5;
-  for (int e = tid; e < H * H; e += NT) {
-    const int i = e / H, k = e % H;
-    Ls[i * XS + k] = (k < i) ? mrow(L, s0 + i)[s0 + k] : 0.0;
+  // Ls (strictly lower part of the factored h x h block) and X (the block above the
+  // destination columns) in 32-byte row segments: s0, d0 are multiples of 4.
+  for (int e = tid; e < H * (H / 4); e += NT) {
+    const int i = e / (H / 4), k = 4 * (e % (H / 4));
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+    if (k < i) ld_v4(mrow(L, s0 + i) + s0 + k, v0, v1, v2, v3);
+    double* q = Ls + i * XS + k;
+    q[0] = k < i ? v0 : 0.0;
+    q[1] = k + 1 < i ? v1 : 0.0;
+    q[2] = k + 2 < i ? v2 : 0.0;
+    q[3] = k + 3 < i ? v3 : 0.0;
   }
-  for (int e = tid; e < H * 8 * NTILE; e += NT) {
-    const int i = e / (8 * NTILE), j = e % (8 * NTILE);
-    X[i * XS + j] = j < nd ? mrow(L, s0 + i)[d0 + j] : 0.0;
+  for (int e = tid; e < H * 2 * NTILE; e += NT) {
+    const int i = e / (2 * NTILE), j = 4 * (e % (2 * NTILE));
+    const double* src = mrow(L, s0 + i) + d0 + j;
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+    if (j + 3 < nd) {
+      ld_v4(src, v0, v1, v2, v3);
+    } else if (j < nd) {
+      v0 = src[0];
+      if (j + 1 < nd) v1 = src[1];
+      if (j + 2 < nd) v2 = src[2];
+    }
+    double* q = X + i * XS + j;
+    q[0] = v0; q[1] = v1; q[2] = v2; q[3] = v3;
   }
   G.sync();
   if (warp == 0 && lane < nd) {  // U part: one column per lane, registers, no barriers
@@ -564,9 +582,16 @@ __device__ void panel_update_t(const Grp& G, const LeafCtx& L, int s0, int d0, i
     for (int i = 0; i < H; ++i) X[i * XS + lane] = x[i];
   }
   G.sync();
-  for (int e = tid; e < H * nd; e += NT) {
-    const int i = e / nd, j = e % nd;
-    mrow(L, s0 + i)[d0 + j] = X[i * XS + j];
+  for (int e = tid; e < H * 2 * NTILE; e += NT) {
+    const int i = e / (2 * NTILE), j = 4 * (e % (2 * NTILE));
+    if (j >= nd) continue;
+    double* dst = mrow(L, s0 + i) + d0 + j;
+    const double* q = X + i * XS + j;
+    if (j + 3 < nd) {
+      st_v4(dst, q[0], q[1], q[2], q[3]);
+    } else {
+      for (int jj = 0; j + jj < nd; ++jj) dst[jj] = q[jj];
+    }
   }
   PHASE_MARK(6);
   // L part with DMMA: rows logical [d0, R) in 8-row groups; each warp keeps UNR groups'
@@ -644,9 +669,15 @@ __device__ void panel_update(const Grp& G, const LeafCtx& L, int s0, int h, int 
 __device__ void panel_linv(const Grp& G, const LeafCtx& L, int c0, int w, double* linv) {
   double* Ls = L.scratch;             // 64 x 65
   const int tid = G.tid, lane = tid & 31, warp = tid >> 5;
-  for (int e = tid; e < 64 * 64; e += NT) {
-    const int i = e >> 6, k = e & 63;
-    Ls[i * 65 + k] = (i < w && k < i) ? mrow(L, c0 + i)[c0 + k] : 0.0;
+  for (int e = tid; e < 64 * 16; e += NT) {
+    const int i = e >> 4, k = 4 * (e & 15);
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+    if (i < w && k < i) ld_v4(mrow(L, c0 + i) + c0 + k, v0, v1, v2, v3);   // c0 % 64 == 0
+    double* q = Ls + i * 65 + k;
+    q[0] = (i < w && k < i) ? v0 : 0.0;
+    q[1] = (i < w && k + 1 < i) ? v1 : 0.0;
+    q[2] = (i < w && k + 2 < i) ? v2 : 0.0;
+    q[3] = (i < w && k + 3 < i) ? v3 : 0.0;
   }
   G.sync();
   // lane (jj, q): column j = jb + 8 warp + jj, rows i = 4 r + q (r < 16).  Rows interleaved by

@@ -132,7 +132,7 @@ struct Smem {
   unsigned long long full[NSTAGE];   // stage filled (256 thread arrivals)
   unsigned long long empty[NSTAGE];  // stage consumed (8 warp arrivals)
   unsigned gchunk;                   // running K-chunk counter of this CTA
-  double wrow[2][NWARP][4];          // per-warp pivot candidate rows (double-buffered)
+  alignas(16) double wrow[2][NWARP][8];          // per-warp pivot candidate rows + 1/pivot (double-buffered)
   unsigned long long redk[2][NWARP];
   short perm[MAX_RPAD];              // logical -> physical row
   short iperm[MAX_RPAD];             // physical -> logical row
@@ -388,7 +388,7 @@ struct LeafCtx {
   short* perm;               // shared: logical -> physical
   short* iperm;              // shared: physical -> logical
   double* scratch;           // shared: panel scratch (>= 64*65 doubles)
-  double* wrow;              // shared: [2][8][4] pivot candidate rows
+  double* wrow;              // shared: [2][NWARP][8] pivot candidate rows, [4] = 1/pivot
   unsigned long long* redk;  // shared: [2][8] pivot keys
 };
 
@@ -446,10 +446,11 @@ __device__ void base_strip(const Grp& G, const LeafCtx& L, int e, int sw, double
   }
   G.sync();  // all perm reads done before thread 0 starts swapping
   PHASE_MARK(8);
+  int pivrow[4];
+  double pivval[4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     if (j >= sw) break;
-    const int col = e + j;
     const int buf = j & 1;
     unsigned long long best = 0ull;
     int bs = 0;
@@ -459,23 +460,23 @@ __device__ void base_strip(const Grp& G, const LeafCtx& L, int e, int sw, double
           ((active >> s) & 1u) && phys[s] < L.ni ? pivot_key(x[s][j], phys[s]) : 0ull;
       if (k > best) { best = k; bs = s; }
     }
-    unsigned long long wbest = best;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const unsigned long long ok = __shfl_xor_sync(0xffffffffu, wbest, o);
-      wbest = ok > wbest ? ok : wbest;
-    }
+    // Warp arg-max of the 64-bit keys with two redux.sync (high word, then low word among
+    // the lanes holding the maximal high word).
+    const unsigned hi = static_cast<unsigned>(best >> 32);
+    const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? static_cast<unsigned>(best) : 0u);
+    const unsigned long long wbest = (static_cast<unsigned long long>(mhi) << 32) | mlo;
     if (lane == 0) L.redk[buf * NWARP + warp] = wbest;
     if (best == wbest && best != 0ull) {  // this lane owns the warp's candidate row
       double r0 = x[0][0], r1 = x[0][1], r2 = x[0][2], r3 = x[0][3];
 #pragma unroll
       for (int s = 1; s < NSLOT; ++s)
         if (s == bs) { r0 = x[s][0]; r1 = x[s][1]; r2 = x[s][2]; r3 = x[s][3]; }
-      double* wr = L.wrow + (buf * NWARP + warp) * 4;
-      wr[0] = r0;
-      wr[1] = r1;
-      wr[2] = r2;
-      wr[3] = r3;
+      const double pv = j == 0 ? r0 : j == 1 ? r1 : j == 2 ? r2 : r3;
+      double* wr = L.wrow + (buf * NWARP + warp) * 8;
+      *reinterpret_cast<double2*>(wr) = make_double2(r0, r1);
+      *reinterpret_cast<double2*>(wr + 2) = make_double2(r2, r3);
+      wr[4] = 1.0 / pv;   // dgetf2-style reciprocal, off the post-barrier critical path
     }
     G.sync();
     unsigned long long kb = L.redk[buf * NWARP];
@@ -486,20 +487,13 @@ __device__ void base_strip(const Grp& G, const LeafCtx& L, int e, int sw, double
       if (k > kb) { kb = k; ww = w; }
     }
     const int pphys = 0x7FF - static_cast<int>(kb & 0x7FFull);
-    double prow[4];
-#pragma unroll
-    for (int jj = 0; jj < 4; ++jj) prow[jj] = L.wrow[(buf * NWARP + ww) * 4 + jj];
-    const double piv = prow[j];
-    const double rpiv = 1.0 / piv;   // dgetf2-style reciprocal scaling
-    if (tid == 0) {
-      minpiv = fmin(minpiv, fabs(piv));
-      const int q = L.iperm[pphys];
-      const int pold = L.perm[col];
-      L.perm[col] = (short)pphys;
-      L.perm[q] = (short)pold;
-      L.iperm[pphys] = (short)col;
-      L.iperm[pold] = (short)q;
-    }
+    const double* wr = L.wrow + (buf * NWARP + ww) * 8;
+    const double2 p01 = *reinterpret_cast<const double2*>(wr);
+    const double2 p23 = *reinterpret_cast<const double2*>(wr + 2);
+    const double rpiv = wr[4];
+    const double prow[4] = {p01.x, p01.y, p23.x, p23.y};
+    pivrow[j] = pphys;
+    pivval[j] = prow[j];
 #pragma unroll
     for (int s = 0; s < NSLOT; ++s) {
       if (phys[s] == pphys) active &= ~(1u << s);
@@ -510,6 +504,21 @@ __device__ void base_strip(const Grp& G, const LeafCtx& L, int e, int sw, double
         for (int jj = 0; jj < 4; ++jj)
           if (jj > j && jj < sw) x[s][jj] = fma(-l, prow[jj], x[s][jj]);
       }
+    }
+  }
+  // Row interchanges (bookkeeping only, in column order) and the pivot minimum, once per strip.
+  if (tid == 0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      if (j >= sw) break;
+      const int col = e + j, pphys = pivrow[j];
+      minpiv = fmin(minpiv, fabs(pivval[j]));
+      const int q = L.iperm[pphys];
+      const int pold = L.perm[col];
+      L.perm[col] = (short)pphys;
+      L.perm[q] = (short)pold;
+      L.iperm[pphys] = (short)col;
+      L.iperm[pold] = (short)q;
     }
   }
   PHASE_MARK(9);
@@ -921,7 +930,7 @@ constexpr int PIPE_LA = cmax(cmax(TileL2::NS * TileL2::STAGE, TileU2::NS * TileU
 struct SmemLA {
   double pipe[PIPE_LA];
   double pan[PAN_DBL];
-  double wrow[2][NT / 32][4];
+  alignas(16) double wrow[2][NT / 32][8];
   unsigned long long redk[2][NT / 32];
   unsigned long long full[MAX_NSTAGE];
   unsigned long long empty[MAX_NSTAGE];

@@ -4,7 +4,7 @@
 NVCC      ?= nvcc
 ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-ffp-contract=off -Iinclude \
-             -Ipaper_2211_14969_b200/csrc -Xptxas -v
+             -Ipaper_2211_14969_b200/csrc -Xptxas -v $(EXTRA)
 SRC       := paper_2211_14969_b200/csrc
 OBJDIR    := build/obj
 LIB       := paper_2211_14969_b200/_lib/libhps_leaf_b200.so

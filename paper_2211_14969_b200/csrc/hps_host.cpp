@@ -388,6 +388,11 @@ void enqueue_condense_chunk(hps_gpu_ctx* ctx, int e, int n, const double* d_b, c
                  (sum[2] + sum[8] + sum[9] + sum[10] + sum[6] + sum[7]) / n,
                  (sum[8] + sum[9] + sum[10]) / n, sum[8] / n, sum[9] / n, sum[10] / n, sum[6] / n,
                  sum[7] / n, sum[3] / n, sum[4] / n);
+    if (sum[11] + sum[12] + sum[13] + sum[14] + sum[15] > 0)
+      std::fprintf(stderr,
+                   "[hps strip column cycles/leaf] keys+redux %.3g  publish %.3g  barrier %.3g  "
+                   "select %.3g  update %.3g\n",
+                   sum[11] / n, sum[12] / n, sum[13] / n, sum[14] / n, sum[15] / n);
   }
 }
 

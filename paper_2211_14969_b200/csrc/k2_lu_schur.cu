@@ -47,6 +47,11 @@ namespace HPS_CFG {
 // Optional per-phase cycle counters (LuArgs::phase_cycles != nullptr): thread 0
 // accumulates clock64() deltas between CTA-wide barriers into 8 slots per leaf:
 // 0 U-part tiles, 1 L-part tiles, 2 panel strips+updates, 3 Linv, 4 trailing.
+#ifdef HPS_STRIP_MARKS
+#define STRIP_MARK(slot) PHASE_MARK(slot)
+#else
+#define STRIP_MARK(slot) do { } while (0)
+#endif
 #define PHASE_MARK(slot)                                                     \
   do {                                                                       \
     if (pc && G.tid == 0) {                                                  \
@@ -346,9 +351,51 @@ __device__ __forceinline__ void acc_store(const Acc& acc, const CRow& crow, int 
 
 // U-part epilogue: acc (64x128 tile) <- Linv (64x64) * acc.  The tile goes through
 // shared memory; Linv fragments come straight from global (32 KB per block row, L1/L2
-// resident across the block row's tiles).
+// resident across the block row's tiles).  TRI = 1: Linv is lower triangular (zeros above
+// the diagonal), TRI = 2: upper; the k-steps that only meet those zeros are skipped
+// (72 of 128 DMMA groups remain).
+constexpr int TRI_FULL = 0, TRI_LOWER = 1, TRI_UPPER = 2;
+#ifndef HPS_NACT
+#define HPS_NACT (HPS_NT == 256)   // skip DMMA on warp tiles made only of column padding
+#endif
+#ifndef HPS_TRI_SKIP
+#define HPS_TRI_SKIP 1
+#endif
+
+// acc = Linv[32 WMI .. 32 WMI + 31, :] * Cs[:, 32 wn ..]: fully unrolled so the triangular
+// k-range of every 8-row group is a compile-time constant.
+template <int TRI, int WMI>
+__device__ __forceinline__ void linv_core(Acc& acc, const double* __restrict__ linv, const double* Cs,
+                                          int wn, int g, int t, int ls) {
+  acc_zero(acc);
+#pragma unroll
+  for (int kk = 0; kk < 16; ++kk) {
+    // rows of group mi: [32 WMI + 8 mi, +8); k-step covers k in [4 kk, 4 kk + 4)
+    bool need[4];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+      need[mi] = !HPS_TRI_SKIP || TRI == TRI_FULL ||
+                 (TRI == TRI_LOWER ? 4 * kk <= 32 * WMI + 8 * mi + 7 : 4 * kk + 3 >= 32 * WMI + 8 * mi);
+    if (!(need[0] || need[1] || need[2] || need[3])) continue;
+    double av[4], bv[4];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+      if (need[mi]) av[mi] = linv[(32 * WMI + 8 * mi + g) * 64 + 4 * kk + t];  // coherent: written in-kernel
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) bv[ni] = Cs[(4 * kk + t) * ls + 32 * wn + 8 * ni + g];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) {
+      if (!need[mi]) continue;
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni) dmma(acc.v[mi][ni][0], acc.v[mi][ni][1], av[mi], bv[ni]);
+    }
+  }
+}
+
+template <int TRI = TRI_FULL>
 __device__ __forceinline__ void linv_apply(const Grp& G, Acc& acc, const double* __restrict__ linv,
                                            double* pipe, int nact = TUN) {
+  static_assert(TileU::WM == 2, "linv_apply: two 32-row warp groups");
   double* Cs = pipe;   // 64 x LS_U
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int wm = warp % TileU::WM, wn = warp / TileU::WM;
@@ -362,19 +409,8 @@ __device__ __forceinline__ void linv_apply(const Grp& G, Acc& acc, const double*
           make_double2(acc.v[mi][ni][0], acc.v[mi][ni][1]);
   G.sync();
   if (act) {
-  acc_zero(acc);
-#pragma unroll 4
-  for (int kk = 0; kk < 16; ++kk) {
-    double av[4], bv[4];
-#pragma unroll
-    for (int mi = 0; mi < 4; ++mi) av[mi] = linv[(32 * wm + 8 * mi + g) * 64 + 4 * kk + t];  // coherent: Linv is written in-kernel
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) bv[ni] = Cs[(4 * kk + t) * LS_U + 32 * wn + 8 * ni + g];
-#pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < 4; ++ni) dmma(acc.v[mi][ni][0], acc.v[mi][ni][1], av[mi], bv[ni]);
-  }
+    if (wm == 0) linv_core<TRI, 0>(acc, linv, Cs, wn, g, t, LS_U);
+    else linv_core<TRI, 1>(acc, linv, Cs, wn, g, t, LS_U);
   }
   G.sync();
 }
@@ -460,25 +496,34 @@ __device__ void base_strip(const Grp& G, const LeafCtx& L, int e, int sw, double
           ((active >> s) & 1u) && phys[s] < L.ni ? pivot_key(x[s][j], phys[s]) : 0ull;
       if (k > best) { best = k; bs = s; }
     }
+    // Every lane takes the reciprocal of its own candidate now, so the FP64 division chain
+    // overlaps the warp arg-max instead of following it (only the winner's is published).
+    double cand = x[0][j];
+#pragma unroll
+    for (int s = 1; s < NSLOT; ++s)
+      if (s == bs) cand = x[s][j];
+    const double rcand = best != 0ull ? 1.0 / cand : 0.0;
     // Warp arg-max of the 64-bit keys with two redux.sync (high word, then low word among
     // the lanes holding the maximal high word).
     const unsigned hi = static_cast<unsigned>(best >> 32);
     const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
     const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? static_cast<unsigned>(best) : 0u);
     const unsigned long long wbest = (static_cast<unsigned long long>(mhi) << 32) | mlo;
+    STRIP_MARK(11);
     if (lane == 0) L.redk[buf * NWARP + warp] = wbest;
     if (best == wbest && best != 0ull) {  // this lane owns the warp's candidate row
       double r0 = x[0][0], r1 = x[0][1], r2 = x[0][2], r3 = x[0][3];
 #pragma unroll
       for (int s = 1; s < NSLOT; ++s)
         if (s == bs) { r0 = x[s][0]; r1 = x[s][1]; r2 = x[s][2]; r3 = x[s][3]; }
-      const double pv = j == 0 ? r0 : j == 1 ? r1 : j == 2 ? r2 : r3;
       double* wr = L.wrow + (buf * NWARP + warp) * 8;
       *reinterpret_cast<double2*>(wr) = make_double2(r0, r1);
       *reinterpret_cast<double2*>(wr + 2) = make_double2(r2, r3);
-      wr[4] = 1.0 / pv;   // dgetf2-style reciprocal, off the post-barrier critical path
+      wr[4] = rcand;   // dgetf2-style reciprocal 1/pivot
     }
+    STRIP_MARK(12);
     G.sync();
+    STRIP_MARK(13);
     unsigned long long kb = L.redk[buf * NWARP];
     int ww = 0;
 #pragma unroll
@@ -494,6 +539,7 @@ __device__ void base_strip(const Grp& G, const LeafCtx& L, int e, int sw, double
     const double prow[4] = {p01.x, p01.y, p23.x, p23.y};
     pivrow[j] = pphys;
     pivval[j] = prow[j];
+    STRIP_MARK(14);
 #pragma unroll
     for (int s = 0; s < NSLOT; ++s) {
       if (phys[s] == pphys) active &= ~(1u << s);
@@ -505,6 +551,7 @@ __device__ void base_strip(const Grp& G, const LeafCtx& L, int e, int sw, double
           if (jj > j && jj < sw) x[s][jj] = fma(-l, prow[jj], x[s][jj]);
       }
     }
+    STRIP_MARK(15);
   }
   // Row interchanges (bookkeeping only, in column order) and the pivot minimum, once per strip.
   if (tid == 0) {
@@ -796,8 +843,9 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
         };
         auto arow = lrow(rt);
         auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + c0; };
+        // columns c0 + w .. c0 + 63 of the last block are A_ii padding (zero): no DMMA there
         tile_mma<TileL>(G, acc, init, arow, brow, c0, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk,
-                        nr);
+                        nr, HPS_NACT ? w : 64);
         acc_store<TileL>(acc, crow, nr, 64);
       }
       __threadfence_block();
@@ -820,10 +868,13 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
       };
       auto arow = lrow(c0);
       auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + ct; };
-      const int nc = min(TUN, ct_end - ct);
+      // Real (non-padding) columns of this tile: A_ii columns end at ni, the trailing block
+      // [A_ib | f] at tb0 + nb + 1; padding columns stay zero without DMMA work.
+      const int real_end = ct + TUN > d.tb0 ? d.tb0 + d.nb + 1 : d.ni;
+      const int nc = HPS_NACT ? min(TUN, real_end - ct) : TUN;
       tile_mma<TileU>(G, acc, init, arow, brow, c0, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk,
                       64, nc);
-      linv_apply(G, acc, li, sm->pipe, nc);
+      linv_apply<TRI_LOWER>(G, acc, li, sm->pipe, nc);
       acc_store<TileU>(acc, crow, w, min(TUN, ct_end - ct));
     }
     __threadfence_block();
@@ -848,7 +899,7 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
       auto arow = lrow(rt);
       auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + c0; };
       tile_mma<TileL>(G, acc, init, arow, brow, d.ni, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk,
-                      nr);
+                      nr, HPS_NACT ? d.nb + 1 - 64 * tb : 64);
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi) {
         const int r = acc_row<TileL>(mi);
@@ -1019,7 +1070,7 @@ __device__ void process_leaf_la(const LuArgs& a, SmemLA* sm, const int leaf, con
       Acc acc;
       auto init = [&](Acc& x) { acc_load<TileU2>(x, crow, 64); };
       tile_mma<TileU2>(G, acc, init, arow, brow, K, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
-      linv_apply(G, acc, Linv + (size_t)J * 4096, sm->pipe);
+      linv_apply<TRI_LOWER>(G, acc, Linv + (size_t)J * 4096, sm->pipe);
       acc_store<TileU2>(acc, crow, w, ncols);
     };
     // column 0 holds original values: panel 0 may start at once
@@ -1052,7 +1103,7 @@ __device__ void process_leaf_la(const LuArgs& a, SmemLA* sm, const int leaf, con
           auto crow = [=](int i) -> double* { return Mw + (size_t)perm[c0 + i] * ld + c1; };
           Acc acc;
           acc_load<TileU2>(acc, crow, 64);
-          linv_apply(G, acc, Linv + (size_t)J * 4096, sm->pipe);
+          linv_apply<TRI_LOWER>(G, acc, Linv + (size_t)J * 4096, sm->pipe);
           acc_store<TileU2>(acc, crow, 64, 64);
         }
         __threadfence_block();
@@ -1214,7 +1265,7 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k3_ssolve_kernel(LuArgs a, do
         Acc acc;
         auto init = [&](Acc& x) { acc_load<TileU>(x, crow, 64); };
         tile_mma<TileU>(G, acc, init, arow, brow, K, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
-        linv_apply(G, acc, uinv, sm->pipe);
+        linv_apply<TRI_UPPER>(G, acc, uinv, sm->pipe);
         acc_store<TileU>(acc, crow, w, min(TUN, ct_end - ct));
       }
       __threadfence_block();

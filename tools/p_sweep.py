@@ -1,0 +1,69 @@
+"""BASELINE config 5 on one GPU: p sweep 8 -> 42 at fixed ~25M DOF (nx = ny = round(5000/(p-1)),
+SURVEY.md §8d C5).  The 8-GPU run shards leaves by range with no collectives, so one GPU's
+work is its 1/8 leaf slice; this measures that slice (device-resident inputs, K1 + K2 device
+time from CUDA events on the launching stream) and reports leaf-stage time, leaves/s, DOF/s
+and achieved FP64 TFLOP/s against the measured DMMA peak.
+
+  python tools/p_sweep.py [--gpus-share 8] [--reps 3] [--out profiles/r01_p_sweep.json]
+"""
+import argparse, json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import torch
+from paper_2211_14969_b200 import leaf_gpu as G, problems as P
+
+PEAK_TF = 37.1   # measured DMMA f64 loop (profiles/r01_fp64_peak.log)
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--ps", default="8,12,16,22,27,32,37,42")
+ap.add_argument("--gpus-share", type=int, default=8)
+ap.add_argument("--kappa", type=float, default=500.0)
+ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--out", default="")
+a = ap.parse_args()
+
+rows = []
+for p in [int(x) for x in a.ps.split(",")]:
+    nx = int(round(5000 / (p - 1)))
+    N = (nx * (p - 1) + 1) ** 2
+    leaves = nx * nx
+    n = (leaves + a.gpus_share - 1) // a.gpus_share       # rank 0's slice
+    X, Y = P.leaf_coords(nx, nx, p, elements=np.arange(n))
+    b = torch.from_numpy(P.crystal_field(X, Y)).cuda()
+    f = torch.zeros_like(b)
+    nb = 4 * (p - 1)
+    T = torch.empty((n, nb, nb), dtype=torch.float64, device="cuda")
+    w = torch.empty((n, nb), dtype=torch.float64, device="cuda")
+    s = torch.empty(n, dtype=torch.int32, device="cuda")
+    st = G.LeafStage(p, nx, nx, a.kappa, a=1.0 / nx)
+    strm = torch.cuda.Stream()
+    best = None
+    for r in range(a.reps + 1):          # first call = warm-up (module load, workspace)
+        st.reset_timing()
+        st.condense_device(0, n, b.data_ptr(), f.data_ptr(), T.data_ptr(), w.data_ptr(), s.data_ptr(),
+                           strm.cuda_stream)
+        tm = st.timing()
+        if r > 0 and (best is None or tm["ms_total"] < best["ms_total"]):
+            best = tm
+    torch.cuda.synchronize()
+    bad = int((s != 0).sum().item())
+    info = st.info()
+    st.close()
+    ms = best["ms_total"]
+    tf = n * P.flops_condense(p) / (ms * 1e-3) / 1e12
+    tf_k2 = n * P.flops_condense(p) / (best["ms_lu_schur"] * 1e-3) / 1e12
+    row = dict(p=p, nx=nx, leaves_total=leaves, dof_total=N, leaves_slice=n, ms_slice=ms,
+               ms_k1=best["ms_assemble"], ms_k2=best["ms_lu_schur"], chunks=best["chunks"],
+               leaves_per_s=n / (ms * 1e-3), dof_per_s_8gpu_equiv=N / (ms * 1e-3),
+               tflops=tf, tflops_k2=tf_k2, frac_peak=tf / PEAK_TF, frac_peak_k2=tf_k2 / PEAK_TF,
+               resident_ctas=info["resident_ctas"], resonant=bad)
+    rows.append(row)
+    print(json.dumps(row), flush=True)
+    del b, f, T, w, s
+    torch.cuda.empty_cache()
+
+if a.out:
+    with open(a.out, "w") as fh:
+        json.dump(dict(config="C5 p sweep, ~25M DOF, kappa=%g, crystal b(x), f=0; 1/%d leaf slice "
+                       "(rank 0 of the leaf-range shard) on one B200" % (a.kappa, a.gpus_share),
+                       peak_tflops=PEAK_TF, rows=rows), fh, indent=1)

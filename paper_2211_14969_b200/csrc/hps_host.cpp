@@ -608,10 +608,19 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
   }
   if (S) CK(ctx->uinv.ensure(size_t(4 * ctx->sms) * 4096 * 8));
   const size_t nis = size_t(d.ni) * d.nb;
+  // Transfer pipeline granularity: at least ~4 chunks (whole waves of resident CTAs) so the
+  // H2D of chunk i+1 and the D2H of chunk i-1 overlap the compute of chunk i even when the
+  // whole range fits the workspace.  'store' keeps one chunk (its factors stay resident).
+  int io_chunk = chunk;
+  if (ctx->desc.storage != HPS_STORAGE_STORE) {
+    const int slots = ctx->k2_ctas * ctx->sms;
+    const int quarter = (e1 - e0 + 3) / 4;
+    io_chunk = std::min(chunk, std::max(slots, (quarter + slots - 1) / slots * slots));
+  }
   reset_timing(ctx);
   int ci = 0;
-  for (int c0 = e0; c0 < e1; c0 += chunk, ++ci) {
-    const int n = std::min(chunk, e1 - c0);
+  for (int c0 = e0; c0 < e1; c0 += io_chunk, ++ci) {
+    const int n = std::min(io_chunk, e1 - c0);
     const int k = ci & 1;
     const size_t off = size_t(c0 - e0);
     CK(cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_in_free[k], 0));
@@ -697,10 +706,19 @@ int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b
     CK(ctx->out_u[i].ensure(size_t(chunk) * pp * 8));
     CK(ctx->out_st[i].ensure(size_t(chunk) * 4));
   }
+  // Transfer pipeline granularity: at least ~4 chunks (whole waves of resident CTAs) so the
+  // H2D of chunk i+1 and the D2H of chunk i-1 overlap the compute of chunk i even when the
+  // whole range fits the workspace.  'store' keeps one chunk (its factors stay resident).
+  int io_chunk = chunk;
+  if (ctx->desc.storage != HPS_STORAGE_STORE) {
+    const int slots = ctx->k2_ctas * ctx->sms;
+    const int quarter = (e1 - e0 + 3) / 4;
+    io_chunk = std::min(chunk, std::max(slots, (quarter + slots - 1) / slots * slots));
+  }
   reset_timing(ctx);
   int ci = 0;
-  for (int c0 = e0; c0 < e1; c0 += chunk, ++ci) {
-    const int n = std::min(chunk, e1 - c0);
+  for (int c0 = e0; c0 < e1; c0 += io_chunk, ++ci) {
+    const int n = std::min(io_chunk, e1 - c0);
     const int k = ci & 1;
     const size_t off = size_t(c0 - e0);
     CK(cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_in_free[k], 0));

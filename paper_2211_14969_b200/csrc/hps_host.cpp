@@ -219,6 +219,10 @@ struct hps_gpu_ctx {
   // HPS_K2_CFG=128|256 forces the K2 build (default: by leaf size, hps_kernels.h use_g128).
   int max_ctas = std::getenv("HPS_K2_CTAS") ? std::atoi(std::getenv("HPS_K2_CTAS")) : 0;
   int force_cfg = std::getenv("HPS_K2_CFG") ? std::atoi(std::getenv("HPS_K2_CFG")) : 0;
+  // K2s (register-resident, assembly fused) where it measured faster (p <= 12, not 10);
+  // HPS_SMALL=0 disables it, HPS_SMALL=1 forces it for every supported p.  The blocked
+  // K1+K2 path still runs where the factors must stay resident (S_solve, 'store').
+  int small_env = std::getenv("HPS_SMALL") ? std::atoi(std::getenv("HPS_SMALL")) : -1;
   DevBuf phase_buf;
   int store_e0 = -1, store_e1 = -1;
 
@@ -322,11 +326,87 @@ void finish_timing(hps_gpu_ctx* ctx) {
 }
 
 // Device pipeline for one chunk of `n` leaves starting at element e (K1 + K2).
+bool use_small(const hps_gpu_ctx* ctx, bool need_factors) {
+  if (ctx->small_env == 0 || need_factors || ctx->fused || ctx->lookahead || ctx->phase_timers) return false;
+  return ctx->small_env == 1 ? hpsg::small_condense_supported(ctx->d.p)
+                             : hpsg::small_condense_preferred(ctx->d.p);
+}
+
 void enqueue_condense_chunk(hps_gpu_ctx* ctx, int e, int n, const double* d_b, const double* d_f,
-                            double* d_T, double* d_w, int* d_status, cudaStream_t st) {
+                            double* d_T, double* d_w, int* d_status, cudaStream_t st,
+                            bool need_factors) {
   const LeafDims& d = ctx->d;
   const int* inj = ctx->has_inject ? ctx->inject_all.as<int>() + e : nullptr;
   const int ci = ctx->tslots++;
+  if (use_small(ctx, need_factors)) {
+    // K2s: one kernel, assembly + norm + elimination + T/w/status (no workspace).
+    ctx->tkernels += 1;
+    cudaEventRecord(ctx->timing_event(3 * ci), st);
+    cudaEventRecord(ctx->timing_event(3 * ci + 1), st);
+    hpsg::SmallArgs a;
+    a.Ds = ctx->Ds.as<double>();
+    a.D2 = ctx->D2.as<double>();
+    a.k2 = ctx->k2;
+    a.b = d_b;
+    a.f = d_f;
+    a.T_out = d_T;
+    a.w_out = d_w;
+    a.status = d_status;
+    a.minratio = ctx->minratio.as<double>();
+    a.norms = ctx->norms.as<double>();
+    a.inject = inj;
+    const bool trace = std::getenv("HPS_K2S_TRACE") != nullptr;
+    const int NW = hpsg::small_condense_warps(d.p);
+    const size_t ntr = size_t(3) * d.ni * NW + d.ni + 2 * NW + 1 + 4 * size_t(d.ni);
+    if (trace) {
+      ctx->phase_buf.ensure(ntr * 8);
+      cudaMemsetAsync(ctx->phase_buf.ptr, 0, ntr * 8, st);
+      a.trace = ctx->phase_buf.as<long long>();
+    }
+    hpsg::launch_small_condense(a, d.p, n, st);
+    cudaEventRecord(ctx->timing_event(3 * ci + 2), st);
+    if (trace) {
+      std::vector<long long> h(ntr);
+      cudaMemcpyAsync(h.data(), ctx->phase_buf.ptr, ntr * 8, cudaMemcpyDeviceToHost, st);
+      cudaStreamSynchronize(st);
+      const long long* pub = h.data() + 3 * size_t(d.ni) * NW;
+      const long long* wst = pub + d.ni;   // warp start, after assembly
+      const long long t0 = wst[0];
+      long long asm_max = 0;
+      for (int q = 0; q < NW; ++q) asm_max = std::max(asm_max, wst[NW + q] - wst[q]);
+      double per = double(pub[d.ni - 1] - pub[0]) / std::max(1, d.ni - 1);
+      double wake = 0, bulk = 0;
+      int nw = 0;
+      for (int k = 0; k < d.ni; ++k)
+        for (int q = 0; q < NW; ++q) {
+          const long long r = h[3 * (size_t(k) * NW + q)], e = h[3 * (size_t(k) * NW + q) + 1];
+          wake += double(r - pub[k]);
+          bulk += double(e - r);
+          ++nw;
+        }
+      std::fprintf(stderr,
+                   "[k2s trace p=%d NW=%d] assembly %lld cyc, steps %d, period %.0f cyc/step, "
+                   "recv-publish %.0f, step body %.0f, total %lld cyc\n",
+                   d.p, NW, asm_max, d.ni, per, wake / nw, bulk / nw, wst[2 * NW] - t0);
+      {
+        const long long* tq = wst + 2 * NW + 1;
+        double e = 0, w2 = 0, pa = 0, pre = 0;
+        for (int k = 1; k < d.ni; ++k) {
+          pre += double(tq[4 * k] - pub[k - 1]);
+          e += double(tq[4 * k + 1] - tq[4 * k]);
+          w2 += double(tq[4 * k + 2] - tq[4 * k + 1]);
+          pa += double(pub[k] - tq[4 * k + 2]);
+        }
+        const double n1 = std::max(1, d.ni - 1);
+        std::fprintf(stderr, "[k2s trace] publish(k-1) -> publish(k) entry %.0f | empty wait %.0f | keys+redux %.0f | "
+                     "l + arrive %.0f\n", pre / n1, e / n1, w2 / n1, pa / n1);
+      }
+      std::fprintf(stderr, "[k2s trace] publish deltas:");
+      for (int k = 1; k < std::min(d.ni, 40); ++k) std::fprintf(stderr, " %lld", pub[k] - pub[k - 1]);
+      std::fprintf(stderr, "\n");
+    }
+    return;
+  }
   ctx->tkernels += ctx->fused ? 2 : 3;
   cudaEventRecord(ctx->timing_event(3 * ci), st);
   if (ctx->fused) {
@@ -631,7 +711,8 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
     CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_out_free[k], 0));
     enqueue_condense_chunk(ctx, c0, n, ctx->in_b[k].as<double>(), ctx->in_f[k].as<double>(),
                            ctx->out_T[k].as<double>(), ctx->out_w[k].as<double>(),
-                           ctx->out_st[k].as<int>(), ctx->s_comp);
+                           ctx->out_st[k].as<int>(), ctx->s_comp,
+                           S != nullptr || ctx->desc.storage == HPS_STORAGE_STORE);
     if (S) {  // K3: S_solve from the factored workspace
       hpsg::LuArgs a3;
       a3.d = d;
@@ -680,7 +761,8 @@ int hps_gpu_condense_device(hps_gpu_ctx* ctx, int32_t e0, int32_t n, const doubl
   for (int c0 = 0; c0 < n; c0 += ctx->chunk, ++ci) {
     const int m = std::min(ctx->chunk, n - c0);
     enqueue_condense_chunk(ctx, e0 + c0, m, d_b + c0 * pp, d_f + c0 * pp, d_T + c0 * nb2,
-                           d_w + size_t(c0) * d.nb, d_status + c0, st);
+                           d_w + size_t(c0) * d.nb, d_status + c0, st,
+                           ctx->desc.storage == HPS_STORAGE_STORE);
     CK(cudaGetLastError());
   }
   return HPS_OK;

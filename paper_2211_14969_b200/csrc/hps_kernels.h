@@ -91,6 +91,27 @@ inline void launch_ssolve(const LuArgs& a, double* S_out, double* uinv_ws, int n
   else g256::launch_ssolve(a, S_out, uinv_ws, n_leaves, st);
 }
 
+// K2s: register-resident condensation of small leaves (p <= 12), assembly fused
+// (k2s_small.cu).  T, w, status, minratio (nullable), ||A_ii|| (nullable) per leaf.
+struct SmallArgs {
+  const double* Ds = nullptr;
+  const double* D2 = nullptr;
+  double k2 = 0.0;
+  const double* b = nullptr;   // p*p per leaf
+  const double* f = nullptr;   // p*p per leaf
+  double* T_out = nullptr;
+  double* w_out = nullptr;
+  int* status = nullptr;
+  double* minratio = nullptr;
+  double* norms = nullptr;
+  const int* inject = nullptr;
+  long long* trace = nullptr;  // diagnostics: clock64 per step of leaf 0 (HPS_K2S_TRACE)
+};
+bool small_condense_supported(int p);
+bool small_condense_preferred(int p);
+int small_condense_warps(int p);
+void launch_small_condense(const SmallArgs& a, int p, int n_leaves, cudaStream_t st);
+
 // K5: back substitution u_i = U^{-1} y (y = L^{-1} P rhs in column tb0) and the
 // local solution vector u (p*p per leaf): interior from the solve, boundary = v.
 void launch_backsolve(const LeafDims& d, const double* ws, const short* perm, const double* v,

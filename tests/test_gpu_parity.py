@@ -275,3 +275,43 @@ def test_s_solve_parity(p, kappa, n):
         _, Dn = O.build_leaf(p, a, kappa, b[e])
         Tchk = Dn[:, bd] + Dn[:, it] @ S[e]
         assert np.linalg.norm(Tchk - T[e]) <= 1e-10 * np.linalg.norm(T[e])
+
+
+@pytest.mark.parametrize("p", [4, 5, 6, 7, 8, 9, 10, 11, 12])
+def test_small_kernel_matches_oracle_and_blocked_path(p, monkeypatch):
+    """K2s (register-resident, fused assembly, p <= 12) against the oracle (1e-10 relFro) and
+    against the blocked K1+K2 path (HPS_SMALL=0); chunk-independent bitwise; crystal b near
+    resonance-free range and f ~ U(-1,1) so w is exercised."""
+    nx, ny, kappa = 7, 5, 4.0 * p
+    X, Y = P.leaf_coords(nx, ny, p)
+    b = P.crystal_field(X * 0.4 + 0.3, Y * 0.4 + 0.3)
+    f = np.random.default_rng(p).uniform(-1, 1, b.shape)
+    ref = O.batched_condense(p, 1.0 / nx, kappa, b, f)
+    monkeypatch.setenv("HPS_SMALL", "1")
+    with G().LeafStage(p, nx, ny, kappa) as st:
+        T1, w1, s1 = st.condense(b, f)
+        T3, w3, _ = st.condense(b[5:17], f[5:17], e0=5)
+    assert not s1.any()
+    assert rel_fro(T1, ref["T"]).max() <= TOL_T
+    assert rel_fro(w1, ref["w"]).max() <= TOL_T
+    assert np.array_equal(T1[5:17].view(np.int64), T3.view(np.int64))
+    assert np.array_equal(w1[5:17].view(np.int64), w3.view(np.int64))
+    monkeypatch.setenv("HPS_SMALL", "0")
+    with G().LeafStage(p, nx, ny, kappa) as st:
+        T2, w2, _ = st.condense(b, f)
+    assert rel_fro(T1, T2).max() <= 1e-12
+    assert rel_fro(w1, w2).max() <= 1e-12
+
+
+@pytest.mark.parametrize("p", [6, 12])
+def test_small_kernel_resonance_injection(p, monkeypatch):
+    monkeypatch.setenv("HPS_SMALL", "1")
+    nx, ny = 4, 3
+    b, f = random_leaves(p, nx * ny, seed=11)
+    with G().LeafStage(p, nx, ny, 3.0) as st:
+        st.set_fault_injection([9, 4, 7])
+        T, w, s = st.condense(b, f, raise_on_resonance=False)
+        assert list(np.nonzero(s)[0]) == [4, 7, 9]
+        r = O.batched_condense(p, 1.0 / nx, 3.0, b, f, inject=[9, 4, 7], raise_on_resonance=False)
+        ok = s == 0
+        assert rel_fro(T[ok], r["T"][ok]).max() <= TOL_T

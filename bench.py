@@ -186,6 +186,13 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def k2_kernel_name(p):
+    """The condensation kernel the C-ABI dispatches for p (hps_kernels.h small_condense_preferred)."""
+    if 4 <= p <= 12 and p != 10 and os.environ.get("HPS_SMALL", "") != "0":
+        return "k2s_condense_kernel (register-resident, fused assembly, DFMA f64)"
+    return "k2_lu_schur_kernel (DMMA f64)"
+
+
 def workload_config(cfg, n_gpus):
     return {"workload": f"{cfg['name']}: batched_condense p={cfg['p']}, {cfg['nx']}x{cfg['ny']} leaves, "
                         f"kappa={cfg['kappa']}, crystal b(x), f=0",
@@ -368,7 +375,7 @@ def main():
             "dof_per_s": value * cfg["N"] / cfg["n_leaves"],
             "tflops": value * f_leaf / 1e12,
             "fp64_peak_frac": value * f_leaf / 1e12 / (FP64_PEAK_TFLOPS * world),
-            "roofline": {"bound": "tensor", "kernel": "k2_lu_schur_kernel (DMMA f64)", "achieved": achieved,
+            "roofline": {"bound": "tensor", "kernel": k2_kernel_name(p), "achieved": achieved,
                          "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
                          "traffic": traffic, "peak_source": FP64_PEAK_NOTE,
                          "flops_per_leaf": f_leaf, "k2_ms_per_step_rank0": k2_ms,

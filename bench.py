@@ -188,7 +188,7 @@ def run_reference(args, cfg):
 
 def k2_kernel_name(p):
     """The condensation kernel the C-ABI dispatches for p (hps_kernels.h small_condense_preferred)."""
-    if 4 <= p <= 12 and p != 10 and os.environ.get("HPS_SMALL", "") != "0":
+    if 4 <= p <= 12 and os.environ.get("HPS_SMALL", "") != "0":
         return "k2s_condense_kernel (register-resident, fused assembly, DFMA f64)"
     return "k2_lu_schur_kernel (DMMA f64)"
 

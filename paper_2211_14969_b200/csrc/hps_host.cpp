@@ -356,8 +356,9 @@ void enqueue_condense_chunk(hps_gpu_ctx* ctx, int e, int n, const double* d_b, c
     a.norms = ctx->norms.as<double>();
     a.inject = inj;
     const bool trace = std::getenv("HPS_K2S_TRACE") != nullptr;
-    const int NW = hpsg::small_condense_warps(d.p);
-    const size_t ntr = size_t(3) * d.ni * NW + d.ni + 2 * NW + 1 + 4 * size_t(d.ni);
+    const int NW = hpsg::small_condense_warps(d.p), BW = hpsg::small_condense_block(d.p);
+    const int NPB = (d.ni + BW - 1) / BW;
+    const size_t ntr = size_t(3) * NPB * NW + NPB + 2 * NW + 1;
     if (trace) {
       ctx->phase_buf.ensure(ntr * 8);
       cudaMemsetAsync(ctx->phase_buf.ptr, 0, ntr * 8, st);
@@ -369,41 +370,27 @@ void enqueue_condense_chunk(hps_gpu_ctx* ctx, int e, int n, const double* d_b, c
       std::vector<long long> h(ntr);
       cudaMemcpyAsync(h.data(), ctx->phase_buf.ptr, ntr * 8, cudaMemcpyDeviceToHost, st);
       cudaStreamSynchronize(st);
-      const long long* pub = h.data() + 3 * size_t(d.ni) * NW;
-      const long long* wst = pub + d.ni;   // warp start, after assembly
+      const long long* pub = h.data() + 3 * size_t(NPB) * NW;   // block published (owner)
+      const long long* wst = pub + NPB;                          // warp start / after assembly
       const long long t0 = wst[0];
       long long asm_max = 0;
       for (int q = 0; q < NW; ++q) asm_max = std::max(asm_max, wst[NW + q] - wst[q]);
-      double per = double(pub[d.ni - 1] - pub[0]) / std::max(1, d.ni - 1);
+      const double per = NPB > 1 ? double(pub[NPB - 1] - pub[0]) / (NPB - 1) : 0.0;
       double wake = 0, bulk = 0;
       int nw = 0;
-      for (int k = 0; k < d.ni; ++k)
+      for (int kb = 0; kb < NPB; ++kb)
         for (int q = 0; q < NW; ++q) {
-          const long long r = h[3 * (size_t(k) * NW + q)], e = h[3 * (size_t(k) * NW + q) + 1];
-          wake += double(r - pub[k]);
+          const long long r = h[3 * (size_t(kb) * NW + q)], e = h[3 * (size_t(kb) * NW + q) + 1];
+          if (r == 0) continue;
+          wake += double(r - pub[kb]);
           bulk += double(e - r);
           ++nw;
         }
       std::fprintf(stderr,
-                   "[k2s trace p=%d NW=%d] assembly %lld cyc, steps %d, period %.0f cyc/step, "
-                   "recv-publish %.0f, step body %.0f, total %lld cyc\n",
-                   d.p, NW, asm_max, d.ni, per, wake / nw, bulk / nw, wst[2 * NW] - t0);
-      {
-        const long long* tq = wst + 2 * NW + 1;
-        double e = 0, w2 = 0, pa = 0, pre = 0;
-        for (int k = 1; k < d.ni; ++k) {
-          pre += double(tq[4 * k] - pub[k - 1]);
-          e += double(tq[4 * k + 1] - tq[4 * k]);
-          w2 += double(tq[4 * k + 2] - tq[4 * k + 1]);
-          pa += double(pub[k] - tq[4 * k + 2]);
-        }
-        const double n1 = std::max(1, d.ni - 1);
-        std::fprintf(stderr, "[k2s trace] publish(k-1) -> publish(k) entry %.0f | empty wait %.0f | keys+redux %.0f | "
-                     "l + arrive %.0f\n", pre / n1, e / n1, w2 / n1, pa / n1);
-      }
-      std::fprintf(stderr, "[k2s trace] publish deltas:");
-      for (int k = 1; k < std::min(d.ni, 40); ++k) std::fprintf(stderr, " %lld", pub[k] - pub[k - 1]);
-      std::fprintf(stderr, "\n");
+                   "[k2s trace p=%d NW=%d BW=%d] assembly %lld cyc, pivot blocks %d, period %.0f cyc/block "
+                   "(%.0f/step), recv-publish %.0f, block body %.0f, total %lld cyc\n",
+                   d.p, NW, BW, asm_max, NPB, per, per / BW, wake / std::max(1, nw), bulk / std::max(1, nw),
+                   wst[2 * NW] - t0);
     }
     return;
   }

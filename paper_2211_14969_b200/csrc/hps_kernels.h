@@ -110,6 +110,7 @@ struct SmallArgs {
 bool small_condense_supported(int p);
 bool small_condense_preferred(int p);
 int small_condense_warps(int p);
+int small_condense_block(int p);   // pivot columns factored per warp block (BW)
 void launch_small_condense(const SmallArgs& a, int p, int n_leaves, cudaStream_t st);
 
 // K5: back substitution u_i = U^{-1} y (y = L^{-1} P rhs in column tb0) and the

@@ -164,6 +164,19 @@ __device__ __forceinline__ long long globaltimer() {
   return t;
 }
 
+// 1/x for a pivot: MUFU.RCP64H seed + two Newton steps, no special-case branch (IEEE
+// division and __drcp_rn carry one, and a CALL to a slow path, on the pivot chain).
+// Relative error ~1 ulp; x is a nonzero finite pivot (a zero or tiny pivot is a
+// resonance and is flagged through min |pivot| / ||A_ii||).
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  double e = __fma_rn(-x, r, 1.0);
+  r = __fma_rn(r, e, r);
+  e = __fma_rn(-x, r, 1.0);
+  return __fma_rn(r, e, r);
+}
+
 // Order-preserving bits of a non-negative double (for integer atomicMax).
 __device__ __forceinline__ unsigned long long dbits(double x) {
   return static_cast<unsigned long long>(__double_as_longlong(x));

@@ -502,7 +502,7 @@ __device__ void base_strip(const Grp& G, const LeafCtx& L, int e, int sw, double
 #pragma unroll
     for (int s = 1; s < NSLOT; ++s)
       if (s == bs) cand = x[s][j];
-    const double rcand = best != 0ull ? 1.0 / cand : 0.0;
+    const double rcand = best != 0ull ? fast_rcp(cand) : 0.0;
     // Warp arg-max of the 64-bit keys with two redux.sync (high word, then low word among
     // the lanes holding the maximal high word).
     const unsigned hi = static_cast<unsigned>(best >> 32);

@@ -215,6 +215,10 @@ struct hps_gpu_ctx {
   // Panel/GEMM lookahead kernel for condense (HPS_LOOKAHEAD=1); the default 2-leaves-per-SM
   // kernel measured faster on C2/C3/C4 in round 1.
   bool lookahead = std::getenv("HPS_LOOKAHEAD") && std::getenv("HPS_LOOKAHEAD")[0] == '1';
+  // Lock-step multi-leaf K2 kernel (4 leaves per CTA, panels aligned): measured faster for
+  // the 4-warp build (C2: 14.05 -> 13.25 ms), slower for the 8-warp build (C3/C4), so by
+  // default only where the 4-warp build runs.  HPS_LOCKSTEP=0/1 disables/forces it.
+  int lockstep_env = std::getenv("HPS_LOCKSTEP") ? std::atoi(std::getenv("HPS_LOCKSTEP")) : -1;
   long long dephase_ns = std::getenv("HPS_DEPHASE_NS") ? std::atoll(std::getenv("HPS_DEPHASE_NS")) : 0;
   // HPS_K2_CFG=128|256 forces the K2 build (default: by leaf size, hps_kernels.h use_g128).
   int max_ctas = std::getenv("HPS_K2_CTAS") ? std::atoi(std::getenv("HPS_K2_CTAS")) : 0;
@@ -420,6 +424,7 @@ void enqueue_condense_chunk(hps_gpu_ctx* ctx, int e, int n, const double* d_b, c
   a.max_ctas_per_sm = ctx->max_ctas;
   a.fused = ctx->fused ? 1 : 0;
   a.lookahead = (ctx->lookahead && !ctx->fused) ? 1 : 0;
+  a.lockstep = ctx->lockstep_env == 1 || (ctx->lockstep_env != 0 && hpsg::use_g128(d, ctx->force_cfg));
   a.rowcode = ctx->rowcode.as<int>();
   a.colcode = ctx->colcode.as<int>();
   a.Ds = ctx->Ds.as<double>();

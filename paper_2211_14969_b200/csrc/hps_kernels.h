@@ -43,6 +43,7 @@ struct LuArgs {
   long long* phase_cycles = nullptr;  // optional 8 counters per leaf (profiling)
   long long dephase_ns = 0;           // start delay of the second CTA on each SM
   int lookahead = 0;                  // condense: panel/GEMM warp-specialised kernel
+  int lockstep = 0;                   // factor: lock-step multi-leaf kernel (panels aligned)
   int max_ctas_per_sm = 0;            // >0: cap the persistent grid below the occupancy
   // Fused first-touch assembly (fused = 1): tile C-inits are evaluated from the
   // operator definition instead of loaded from a K1-materialised workspace.

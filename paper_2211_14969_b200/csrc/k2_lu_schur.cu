@@ -85,6 +85,10 @@ constexpr int MAX_RPAD = HPS_MAX_ROWS + 128;  // perm entries (tile gathers may 
 // A group of 256 threads (8 warps) sharing a named barrier.  The one-leaf-per-CTA kernel
 // uses the whole CTA (barrier 0); the lookahead kernel runs a GEMM group (threads 0-255,
 // barrier 1) and a panel group (threads 256-511, barrier 2) side by side.
+// Thread index within its group of NT threads (the tile/panel helpers are group-local:
+// one-leaf kernel, lookahead kernel groups, lock-step multi-leaf kernel groups).
+__device__ __forceinline__ int gtid() { return static_cast<int>(threadIdx.x) & (NT - 1); }
+
 struct Grp {
   int tid;   // thread index within the group
   int bar;   // named barrier id
@@ -150,12 +154,12 @@ struct Acc {
 
 template <class TL>
 __device__ __forceinline__ int acc_row(int mi) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = gtid() >> 5, lane = threadIdx.x & 31;
   return 32 * (warp % TL::WM) + 8 * mi + (lane >> 2);
 }
 template <class TL>
 __device__ __forceinline__ int acc_col(int ni) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = gtid() >> 5, lane = threadIdx.x & 31;
   return 32 * (warp / TL::WM) + 8 * ni + 2 * (lane & 3);
 }
 
@@ -171,7 +175,7 @@ __device__ __forceinline__ void load_chunk(double* st, unsigned long long* full,
                                            const ARow& arow, const BRow& brow, int k0, int K) {
   double* As = st;
   double* Bs = st + (TL::WM * 32) * TL::LDA;
-  const int tid = threadIdx.x;
+  const int tid = gtid();
   constexpr int TM_ = TL::WM * 32, TN_ = TL::WN * 32, KC_ = TL::K;
   if (k0 + KC_ <= K) {
 #pragma unroll
@@ -214,7 +218,7 @@ __device__ void tile_mma(const Grp& G, Acc& acc, const Init& init, const ARow& a
     init(acc);
     return;
   }
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = gtid() >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const int wm = warp % TL::WM, wn = warp / TL::WM;
   // Warps whose 32x32 tile lies wholly in the padding of a remainder tile (fewer than
@@ -224,7 +228,7 @@ __device__ void tile_mma(const Grp& G, Acc& acc, const Init& init, const ARow& a
   const double* pa[TL::AGR];
 #pragma unroll
   for (int r = 0; r < TL::AGR; ++r) {
-    const int gi = threadIdx.x + r * NT;
+    const int gi = gtid() + r * NT;
     pa[r] = arow(gi / (KC_ / 2)) + 2 * (gi % (KC_ / 2));
   }
   auto fill = [&](int c) {
@@ -397,7 +401,7 @@ __device__ __forceinline__ void linv_apply(const Grp& G, Acc& acc, const double*
                                            double* pipe, int nact = TUN) {
   static_assert(TileU::WM == 2, "linv_apply: two 32-row warp groups");
   double* Cs = pipe;   // 64 x LS_U
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+  const int warp = gtid() >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   const int wm = warp % TileU::WM, wn = warp / TileU::WM;
   const bool act = 32 * wn < nact;   // each warp reads only its own 32 columns of Cs
   if (act)
@@ -779,9 +783,17 @@ __device__ void panel_factor(const Grp& G, const LeafCtx& L, int c0, int w, doub
 // ---------------------------------------------------------------------------
 // Kernel
 // ---------------------------------------------------------------------------
+// lock_nt > 0 (lock-step multi-leaf kernel): before every panel all groups of the CTA meet
+// at named barrier 15 (lock_nt threads), so the co-resident leaves factor their panels at
+// the same time and run their tile jobs at the same time: the latency-bound panels' scalar
+// FP64 work then does not queue behind the other leaves' DMMA streams.
+__device__ __forceinline__ void lock_sync(int lock_nt) {
+  if (lock_nt > 0) asm volatile("bar.sync 15, %0;\n" ::"r"(lock_nt) : "memory");
+}
+
 template <int NSLOT>
-__device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
-  const Grp G{(int)threadIdx.x, 0};
+__device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf, const Grp G = Grp{(int)threadIdx.x, 0},
+                             int lock_nt = 0) {
   const LeafDims d = a.d;
   LeafCtx L;
   L.M = a.ws + (size_t)leaf * d.leaf_stride;
@@ -797,7 +809,7 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
   short* perm_g = a.perm + (size_t)leaf * d.Rpad;
   // Entries past Rpad are read by masked-out tile rows (e.g. the D-row tiles start at ni, which
   // need not be 64-aligned): point them at a valid row so the gathers stay in bounds.
-  for (int i = threadIdx.x; i < MAX_RPAD; i += NT) {
+  for (int i = G.tid; i < MAX_RPAD; i += NT) {
     sm->perm[i] = i < d.Rpad ? (a.factor ? (short)i : perm_g[i]) : (short)(d.Rpad - 1);
     sm->iperm[i] = (short)i;   // only used while factoring (perm starts as the identity)
   }
@@ -850,6 +862,7 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
       }
       __threadfence_block();
       G.sync();
+      lock_sync(lock_nt);
       PHASE_MARK(1);
       panel_factor<NSLOT>(G, L, c0, w, minpiv, pc, t_phase);
       PHASE_MARK(2);
@@ -924,8 +937,8 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf) {
     return;
   }
   G.sync();
-  for (int i = threadIdx.x; i < d.Rpad; i += NT) perm_g[i] = sm->perm[i];
-  if (threadIdx.x == 0) {
+  for (int i = G.tid; i < d.Rpad; i += NT) perm_g[i] = sm->perm[i];
+  if (G.tid == 0) {
     const double nrm = a.norms[leaf];
     const double ratio = nrm > 0.0 ? minpiv / nrm : 0.0;
     if (a.minratio) a.minratio[leaf] = ratio;
@@ -957,6 +970,39 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k2_lu_schur_kernel(LuArgs a, 
     while (globaltimer() - t0 < a.dephase_ns) __nanosleep(20000);
   }
   for (int leaf = blockIdx.x; leaf < n_leaves; leaf += gridDim.x) process_leaf<NSLOT>(a, sm, leaf);
+}
+
+// Lock-step multi-leaf kernel: one CTA per SM with CTAS_PER_SM groups of NT threads, each
+// group a leaf (own shared-memory slice, pipeline mbarriers and named barrier 1 + group),
+// all groups aligned before every panel (process_leaf lock_nt).  Groups without a leaf in
+// the last round still meet the lock barriers (nblk of them per leaf of the round).
+constexpr int NGRP = CTAS_PER_SM;
+constexpr size_t SMEM_GRP = (sizeof(Smem) + 127) / 128 * 128;
+
+template <int NSLOT>
+__global__ void __launch_bounds__(NT * NGRP, 1) k2_lu_lockstep_kernel(LuArgs a, int n_leaves) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int grp = threadIdx.x / NT;
+  Smem* sm = reinterpret_cast<Smem*>(smem_raw + grp * SMEM_GRP);
+  const Grp G{gtid(), 1 + grp};
+  if (G.tid == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(&sm->full[s], NT);
+      mbar_init(&sm->empty[s], NT / 32);
+    }
+    sm->gchunk = 0;
+  }
+  __syncthreads();
+  const int per_round = gridDim.x * NGRP;
+  for (int base = 0; base < n_leaves; base += per_round) {
+    const int in_round = min(per_round, n_leaves - base);
+    // leaves of this CTA in this round: base + blockIdx.x * NGRP + [0, NGRP) ∩ [0, in_round)
+    const int first = blockIdx.x * NGRP;
+    const int mine = max(0, min(NGRP, in_round - first));
+    if (mine == 0) break;   // no later round has leaves for this CTA either
+    const int lock_nt = NT * mine;
+    if (grp < mine) process_leaf<NSLOT>(a, sm, base + first + grp, G, a.factor && mine > 1 ? lock_nt : 0);
+  }
 }
 
 #if HPS_NT == 256
@@ -1304,6 +1350,14 @@ static void launch_ns(const LuArgs& a, int n_leaves, cudaStream_t st) {
     return;
   }
 #endif
+  if (a.lockstep && a.factor) {
+    const int smem = int(SMEM_GRP * NGRP);
+    cudaFuncSetAttribute(k2_lu_lockstep_kernel<NSLOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int need = (n_leaves + NGRP - 1) / NGRP;
+    const int grid = need < sms ? need : sms;
+    k2_lu_lockstep_kernel<NSLOT><<<grid, NT * NGRP, smem, st>>>(a, n_leaves);
+    return;
+  }
   cudaFuncSetAttribute(k2_lu_schur_kernel<NSLOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)sizeof(Smem));
   // Persistent grid = what is actually co-resident (a grid larger than that would leave

@@ -315,3 +315,26 @@ def test_small_kernel_resonance_injection(p, monkeypatch):
         r = O.batched_condense(p, 1.0 / nx, 3.0, b, f, inject=[9, 4, 7], raise_on_resonance=False)
         ok = s == 0
         assert rel_fro(T[ok], r["T"][ok]).max() <= TOL_T
+
+
+@pytest.mark.parametrize("p", [16, 22])
+def test_lockstep_kernel_bitwise_equals_persistent(p, monkeypatch):
+    """The lock-step multi-leaf K2 kernel runs the same per-leaf code as the one-leaf-per-CTA
+    persistent kernel: T, w bitwise equal (HPS_LOCKSTEP=1 vs 0), including a partial last
+    round (leaf count not a multiple of 4 x #SM) and a single-leaf call."""
+    nx, ny, kappa = 7, 3, 5.0 * p
+    X, Y = P.leaf_coords(nx, ny, p)
+    b = P.crystal_field(X * 0.4 + 0.3, Y * 0.4 + 0.3)
+    f = np.random.default_rng(p).uniform(-1, 1, b.shape)
+    out = {}
+    for ls in ("0", "1"):
+        monkeypatch.setenv("HPS_LOCKSTEP", ls)
+        with G().LeafStage(p, nx, ny, kappa) as st:
+            T, w, s = st.condense(b, f)
+            T1, w1, _ = st.condense(b[3:4], f[3:4], e0=3)
+        assert not s.any()
+        out[ls] = (T, w, T1, w1)
+    for x, y in zip(out["0"], out["1"]):
+        assert np.array_equal(x.view(np.int64), y.view(np.int64))
+    ref = O.batched_condense(p, 1.0 / nx, kappa, b, f)
+    assert rel_fro(out["1"][0], ref["T"]).max() <= TOL_T

@@ -70,19 +70,42 @@ __global__ void __launch_bounds__(256) k4_values_kernel(MeshDev m, const double*
     }
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < q * rowlen; e += blockDim.x) {
-    const int k = e / rowlen, pos = e % rowlen;
-    const int rank = pos / q, kk = pos % q;
-    double v = 0.0;
+  // Four entries per thread per pass, all eight T loads issued before any sum/store
+  // (memory-level parallelism: the loop is HBM-latency bound otherwise).
+  constexpr int U = 4;
+  const int total = q * rowlen;
+  for (int e0 = threadIdx.x; e0 < total; e0 += U * blockDim.x) {
+    double tv[U][2];
+    bool has[U][2];
 #pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const int sc = col_side[t][rank];
-      if (sc >= 0) {
-        const int r = side_base(p, sd[t]) + k;
-        v = __dadd_rn(v, __ldg(T + ((size_t)el[t] * nb + r) * nb + side_base(p, sc) + kk));
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * blockDim.x;
+      has[u][0] = has[u][1] = false;
+      tv[u][0] = tv[u][1] = 0.0;
+      if (e < total) {
+        const int k = e / rowlen, pos = e - k * rowlen;
+        const int rank = pos / q, kk = pos - rank * q;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int sc = col_side[t][rank];
+          if (sc >= 0) {
+            const int r = side_base(p, sd[t]) + k;
+            tv[u][t] = __ldg(T + ((size_t)el[t] * nb + r) * nb + side_base(p, sc) + kk);
+            has[u][t] = true;
+          }
+        }
       }
     }
-    values[off + e] = v;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * blockDim.x;
+      if (e < total) {
+        double v = 0.0;   // 0 + T_e0 + T_e1 in the oracle's order (present terms only)
+        if (has[u][0]) v = __dadd_rn(v, tv[u][0]);
+        if (has[u][1]) v = __dadd_rn(v, tv[u][1]);
+        values[off + e] = v;
+      }
+    }
   }
   // rhs: one thread per row of this edge
   const int Nx = m.nx * (p - 1) + 1, Ny = m.ny * (p - 1) + 1;

@@ -103,6 +103,15 @@ int hps_gpu_condense_device(hps_gpu_ctx* ctx, int32_t e0, int32_t n, const doubl
                             const double* d_f, double* d_T, double* d_w, int32_t* d_status,
                             void* stream);
 
+/* Device-side sampling of the crystal coefficient field (SPEC.md:209-217,
+ * problems.crystal_field) at the p*p local nodes of elements
+ * [e0, e0+n) into d_b (leaf-major, the layout hps_gpu_condense_device reads):
+ *   b = clamp(1 - sum_i depth exp(-|x - c_i|^2 / sigma^2), 0, 1)
+ * with the ncent centres c_i given as (x, y) pairs in host memory.  Enqueued on
+ * `stream` (NULL = ctx stream).  Replaces the host sampling + H2D of b. */
+int hps_gpu_sample_crystal(hps_gpu_ctx* ctx, int32_t e0, int32_t n, const double* centres, int32_t ncent,
+                           double sigma, double depth, double* d_b, void* stream);
+
 /* Batched leaf_solve for elements [e0, e1): u = p*p local
  * values, interior = A_ii^{-1}(f_i - A_ib v), boundary = v.  Recompute policy
  * rebuilds and refactors A_ii; store policy reuses the

@@ -228,6 +228,7 @@ struct hps_gpu_ctx {
   // K1+K2 path still runs where the factors must stay resident (S_solve, 'store').
   int small_env = std::getenv("HPS_SMALL") ? std::atoi(std::getenv("HPS_SMALL")) : -1;
   DevBuf phase_buf;
+  DevBuf field_off, field_cent;   // K0 crystal sampler: node offsets, centres
   int store_e0 = -1, store_e1 = -1;
 
   ~hps_gpu_ctx() {
@@ -757,6 +758,32 @@ int hps_gpu_condense_device(hps_gpu_ctx* ctx, int32_t e0, int32_t n, const doubl
                            ctx->desc.storage == HPS_STORAGE_STORE);
     CK(cudaGetLastError());
   }
+  return HPS_OK;
+}
+
+int hps_gpu_sample_crystal(hps_gpu_ctx* ctx, int32_t e0, int32_t n, const double* centres, int32_t ncent,
+                           double sigma, double depth, double* d_b, void* stream) {
+  if (!ctx) return HPS_ERR_PARAM;
+  if (int rc = check_range(ctx, e0, e0 + n)) return rc;
+  if (!d_b || (ncent > 0 && !centres) || ncent < 0 || !(sigma > 0.0))
+    return ctx->fail(HPS_ERR_PARAM, "ParameterError: crystal sampler needs d_b, centres and sigma > 0");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->s_comp;
+  const int p = ctx->d.p;
+  const double a = ctx->desc.a;
+  // off[k] = (x_k + 1) * (a / 2), x_k the ascending CGL nodes (problems.leaf_coords).
+  std::vector<double> off(p);
+  const double den = 2.0 * double(p - 1);
+  for (int k = 0; k < p; ++k) off[k] = (std::sin(M_PI * double(2 * k - (p - 1)) / den) + 1.0) * (a / 2.0);
+  CK(ctx->field_off.ensure(size_t(p) * 8));
+  CK(ctx->field_cent.ensure(size_t(std::max(1, ncent)) * 16));
+  CK(cudaMemcpyAsync(ctx->field_off.ptr, off.data(), size_t(p) * 8, cudaMemcpyHostToDevice, st));
+  if (ncent > 0)
+    CK(cudaMemcpyAsync(ctx->field_cent.ptr, centres, size_t(ncent) * 16, cudaMemcpyHostToDevice, st));
+  hpsg::launch_crystal(p, ctx->desc.nx, a, ctx->field_off.as<double>(), ctx->field_cent.as<double>(), ncent,
+                       1.0 / (sigma * sigma), depth, e0, n, d_b, st);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(st));   // the host tables above are pageable temporaries
   return HPS_OK;
 }
 

@@ -8,6 +8,11 @@
 
 namespace hpsg {
 
+// K0: crystal-field b(x) samples of leaves [e0, e0+n) (k0_fields.cu); off = (xh+1)*(a/2),
+// centres = 2*ncent doubles (cx, cy), inv_s2 = 1/sigma^2.
+void launch_crystal(int p, int nx, double a, const double* off, const double* centres, int ncent,
+                    double inv_s2, double depth, int e0, int n, double* b, cudaStream_t st);
+
 // K1: augmented leaf matrices + ||A_ii||_inf.
 void launch_assemble(const LeafDims& d, const int* rowcode, const int* colcode, const double* Ds,
                      const double* D2, double k2, const double* b, const double* f, double* ws,

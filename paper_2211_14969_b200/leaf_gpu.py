@@ -58,7 +58,8 @@ _lib = None
 EXPORTED = ["hps_gpu_create", "hps_gpu_destroy", "hps_gpu_last_error", "hps_gpu_get_info",
             "hps_gpu_get_timing", "hps_gpu_reset_timing", "hps_gpu_condense", "hps_gpu_condense_device", "hps_gpu_leaf_solve",
             "hps_gpu_reduced_pattern", "hps_gpu_assemble_reduced", "hps_gpu_assemble_reduced_device",
-            "hps_gpu_set_fault_injection", "hps_host_alloc", "hps_host_free", "hps_gpu_version"]
+            "hps_gpu_set_fault_injection", "hps_host_alloc", "hps_host_free", "hps_gpu_version",
+            "hps_gpu_sample_crystal"]
 
 
 def lib():
@@ -79,7 +80,8 @@ def lib():
         for name in ("hps_gpu_condense", "hps_gpu_condense_device", "hps_gpu_leaf_solve",
                      "hps_gpu_reduced_pattern", "hps_gpu_assemble_reduced",
                      "hps_gpu_assemble_reduced_device", "hps_gpu_set_fault_injection",
-                     "hps_gpu_get_info", "hps_gpu_get_timing", "hps_gpu_reset_timing"):
+                     "hps_gpu_get_info", "hps_gpu_get_timing", "hps_gpu_reset_timing",
+                     "hps_gpu_sample_crystal"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -183,6 +185,17 @@ class LeafStage:
         """Device-resident variant: arguments are raw device pointers (ints)."""
         rc = lib().hps_gpu_condense_device(self._h, e0, n, C.c_void_p(d_b), C.c_void_p(d_f), C.c_void_p(d_T),
                                            C.c_void_p(d_w), C.c_void_p(d_status), C.c_void_p(stream))
+        self._check(rc)
+
+    def sample_crystal_device(self, e0, n, d_b, centres=None, sigma=0.02, depth=0.9, stream=0):
+        """Device-side crystal b(x) samples of elements [e0, e0+n) into the device buffer d_b
+        (raw pointer), the layout condense_device reads."""
+        if centres is None:
+            from . import problems
+            centres = problems.crystal_centres()
+        c = np.ascontiguousarray(np.asarray(centres, dtype=np.float64).reshape(-1, 2))
+        rc = lib().hps_gpu_sample_crystal(self._h, e0, n, _ptr(c), c.shape[0], C.c_double(sigma),
+                                          C.c_double(depth), C.c_void_p(d_b), C.c_void_p(stream))
         self._check(rc)
 
     # -- leaf_solve ---------------------------------------------------------------------------

@@ -338,3 +338,28 @@ def test_lockstep_kernel_bitwise_equals_persistent(p, monkeypatch):
         assert np.array_equal(x.view(np.int64), y.view(np.int64))
     ref = O.batched_condense(p, 1.0 / nx, kappa, b, f)
     assert rel_fro(out["1"][0], ref["T"]).max() <= TOL_T
+
+
+@pytest.mark.parametrize("cfg_name,n", [("C2", 2297), ("C4", 300)])
+def test_device_crystal_sampler(cfg_name, n):
+    """K0: device-side crystal b(x) at every leaf node equals the host
+    restatement problems.crystal_field to the last ulps (exp/sin may differ by 1 ulp), and
+    condensing from device-sampled b matches condensing from host-sampled b."""
+    import torch
+    cfg = P.config(cfg_name)
+    p, nx, ny = cfg["p"], cfg["nx"], cfg["ny"]
+    e0 = 7
+    X, Y = P.leaf_coords(nx, ny, p, a=cfg["a"], elements=np.arange(e0, e0 + n))
+    b_host = P.crystal_field(X, Y)
+    with G().LeafStage(p, nx, ny, cfg["kappa"], a=cfg["a"]) as st:
+        d_b = torch.empty((n, p * p), dtype=torch.float64, device="cuda")
+        st.sample_crystal_device(e0, n, d_b.data_ptr())
+        torch.cuda.synchronize()
+        b_dev = d_b.cpu().numpy()
+        assert np.abs(b_dev - b_host).max() <= 1e-14
+        assert b_dev.min() >= 0.0 and b_dev.max() <= 1.0
+        m = min(n, 64)
+        f = np.zeros((m, p * p))
+        T1, w1, _ = st.condense(b_host[:m], f, e0=e0)
+        T2, w2, _ = st.condense(b_dev[:m], f, e0=e0)
+    assert rel_fro(T2, T1).max() <= 1e-12

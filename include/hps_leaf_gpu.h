@@ -112,6 +112,19 @@ int hps_gpu_condense_device(hps_gpu_ctx* ctx, int32_t e0, int32_t n, const doubl
 int hps_gpu_sample_crystal(hps_gpu_ctx* ctx, int32_t e0, int32_t n, const double* centres, int32_t ncent,
                            double sigma, double depth, double* d_b, void* stream);
 
+/* Matrix-free residual of the global collocation system (SPEC.md:337-342,354-362,
+ * Eq. 7) for the whole mesh, from leaf-major b, f and local
+ * solutions u (p*p per leaf, e.g. hps_gpu_leaf_solve's output):
+ *   out[0] = sum over interior rows of (A_loc u - f)^2,
+ *   out[1] = sum over active interface rows of (sum of the two outward fluxes)^2,
+ *   out[2] = sum over interior rows of f^2.
+ * Dirichlet / interior-corner rows are identity rows, satisfied by construction;
+ * relerr_res = sqrt((out[0] + out[1]) / (out[2] + sum g^2)).  Partials are summed in a
+ * fixed order: bitwise reproducible.  Host-buffer and device-buffer variants. */
+int hps_gpu_residual(hps_gpu_ctx* ctx, const double* b, const double* f, const double* u, double* out);
+int hps_gpu_residual_device(hps_gpu_ctx* ctx, const double* d_b, const double* d_f, const double* d_u,
+                            double* out, void* stream);
+
 /* Batched leaf_solve for elements [e0, e1): u = p*p local
  * values, interior = A_ii^{-1}(f_i - A_ib v), boundary = v.  Recompute policy
  * rebuilds and refactors A_ii; store policy reuses the

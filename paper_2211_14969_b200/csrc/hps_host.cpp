@@ -229,6 +229,7 @@ struct hps_gpu_ctx {
   int small_env = std::getenv("HPS_SMALL") ? std::atoi(std::getenv("HPS_SMALL")) : -1;
   DevBuf phase_buf;
   DevBuf field_off, field_cent;   // K0 crystal sampler: node offsets, centres
+  DevBuf res_flux, res_pl, res_pe, res_in;   // K6 residual scratch
   int store_e0 = -1, store_e1 = -1;
 
   ~hps_gpu_ctx() {
@@ -785,6 +786,49 @@ int hps_gpu_sample_crystal(hps_gpu_ctx* ctx, int32_t e0, int32_t n, const double
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(st));   // the host tables above are pageable temporaries
   return HPS_OK;
+}
+
+int hps_gpu_residual_device(hps_gpu_ctx* ctx, const double* d_b, const double* d_f, const double* d_u,
+                            double* out, void* stream) {
+  if (!ctx) return HPS_ERR_PARAM;
+  if (!d_b || !d_f || !d_u || !out) return ctx->fail(HPS_ERR_PARAM, "ParameterError: null buffer");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->s_comp;
+  const int n = ctx->n_leaves, nb = ctx->d.nb;
+  const int ne = ctx->mesh.n_edges;
+  CK(ctx->res_flux.ensure(size_t(n) * nb * 8));
+  CK(ctx->res_pl.ensure(size_t(n) * 16));
+  CK(ctx->res_pe.ensure(size_t(std::max(1, ne)) * 8));
+  hpsg::launch_residual(ctx->mesh_dev(), ctx->k2, ctx->D2.as<double>(), ctx->Ds.as<double>(), d_b, d_f, d_u,
+                        ctx->res_flux.as<double>(), ctx->res_pl.as<double>(), ctx->res_pe.as<double>(), n, st);
+  CK(cudaGetLastError());
+  std::vector<double> pl(size_t(n) * 2), pe(size_t(std::max(0, ne)));
+  CK(cudaMemcpyAsync(pl.data(), ctx->res_pl.ptr, pl.size() * 8, cudaMemcpyDeviceToHost, st));
+  if (ne > 0) CK(cudaMemcpyAsync(pe.data(), ctx->res_pe.ptr, pe.size() * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  double ri = 0.0, fi = 0.0, rf = 0.0;   // fixed order: elements, then edges
+  for (int e = 0; e < n; ++e) {
+    ri += pl[2 * size_t(e)];
+    fi += pl[2 * size_t(e) + 1];
+  }
+  for (int k = 0; k < ne; ++k) rf += pe[k];
+  out[0] = ri;
+  out[1] = rf;
+  out[2] = fi;
+  return HPS_OK;
+}
+
+int hps_gpu_residual(hps_gpu_ctx* ctx, const double* b, const double* f, const double* u, double* out) {
+  if (!ctx) return HPS_ERR_PARAM;
+  if (!b || !f || !u || !out) return ctx->fail(HPS_ERR_PARAM, "ParameterError: null buffer");
+  CK(cudaSetDevice(ctx->device));
+  const size_t pp = size_t(ctx->d.p) * ctx->d.p, n = size_t(ctx->n_leaves);
+  CK(ctx->res_in.ensure(3 * n * pp * 8));
+  double* d = ctx->res_in.as<double>();
+  CK(cudaMemcpyAsync(d, b, n * pp * 8, cudaMemcpyHostToDevice, ctx->s_comp));
+  CK(cudaMemcpyAsync(d + n * pp, f, n * pp * 8, cudaMemcpyHostToDevice, ctx->s_comp));
+  CK(cudaMemcpyAsync(d + 2 * n * pp, u, n * pp * 8, cudaMemcpyHostToDevice, ctx->s_comp));
+  return hps_gpu_residual_device(ctx, d, d + n * pp, d + 2 * n * pp, out, ctx->s_comp);
 }
 
 int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, const double* f,

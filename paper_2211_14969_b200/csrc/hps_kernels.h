@@ -139,4 +139,11 @@ void launch_reduced_pattern(const MeshDev& m, int64_t* row_ptr, int32_t* col_idx
 void launch_reduced_values(const MeshDev& m, const double* T, const double* w, const double* g_bnd,
                            double* values, double* rhs, cudaStream_t st);
 
+// K6: matrix-free residual of the global collocation system (k6_residual.cu): per-leaf
+// [sum r_int^2, sum f_int^2] into part_leaf (2 per leaf), per-edge sum r_flux^2 into
+// part_edge, outward fluxes (nb per leaf) into the flux scratch.
+void launch_residual(const MeshDev& m, double k2, const double* D2, const double* Ds, const double* b,
+                     const double* f, const double* u, double* flux, double* part_leaf, double* part_edge,
+                     int n_leaves, cudaStream_t st);
+
 }  // namespace hpsg

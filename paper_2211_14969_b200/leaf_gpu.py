@@ -59,7 +59,7 @@ EXPORTED = ["hps_gpu_create", "hps_gpu_destroy", "hps_gpu_last_error", "hps_gpu_
             "hps_gpu_get_timing", "hps_gpu_reset_timing", "hps_gpu_condense", "hps_gpu_condense_device", "hps_gpu_leaf_solve",
             "hps_gpu_reduced_pattern", "hps_gpu_assemble_reduced", "hps_gpu_assemble_reduced_device",
             "hps_gpu_set_fault_injection", "hps_host_alloc", "hps_host_free", "hps_gpu_version",
-            "hps_gpu_sample_crystal"]
+            "hps_gpu_sample_crystal", "hps_gpu_residual", "hps_gpu_residual_device"]
 
 
 def lib():
@@ -81,7 +81,7 @@ def lib():
                      "hps_gpu_reduced_pattern", "hps_gpu_assemble_reduced",
                      "hps_gpu_assemble_reduced_device", "hps_gpu_set_fault_injection",
                      "hps_gpu_get_info", "hps_gpu_get_timing", "hps_gpu_reset_timing",
-                     "hps_gpu_sample_crystal"):
+                     "hps_gpu_sample_crystal", "hps_gpu_residual", "hps_gpu_residual_device"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -197,6 +197,15 @@ class LeafStage:
         rc = lib().hps_gpu_sample_crystal(self._h, e0, n, _ptr(c), c.shape[0], C.c_double(sigma),
                                           C.c_double(depth), C.c_void_p(d_b), C.c_void_p(stream))
         self._check(rc)
+
+    def residual(self, b, f, u_leaf):
+        """Matrix-free residual pieces of the global collocation system for local solutions
+        u_leaf (n_leaves x p^2): dict(r_int2, r_flux2, f_int2) (Eq. 7)."""
+        pp = self.p * self.p
+        b = _f64(b, (-1, pp)); f = _f64(f, (-1, pp)); u = _f64(u_leaf, (-1, pp))
+        out = np.zeros(3)
+        self._check(lib().hps_gpu_residual(self._h, _ptr(b), _ptr(f), _ptr(u), _ptr(out)))
+        return dict(r_int2=out[0], r_flux2=out[1], f_int2=out[2])
 
     # -- leaf_solve ---------------------------------------------------------------------------
     def leaf_solve(self, b, f, v, e0=0):

@@ -363,3 +363,54 @@ def test_device_crystal_sampler(cfg_name, n):
         T1, w1, _ = st.condense(b_host[:m], f, e0=e0)
         T2, w2, _ = st.condense(b_dev[:m], f, e0=e0)
     assert rel_fro(T2, T1).max() <= 1e-12
+
+
+@pytest.mark.parametrize("n,p,kappa", [(2, 6, 3.0), (3, 8, 10.0), (4, 10, 2 * math.pi)])
+def test_residual_matches_dense_global_system(n, p, kappa):
+    """K6: the matrix-free device residual of the global collocation system
+    equals the dense assemble_global residual, row class by row class, for an arbitrary
+    (non-solution) globally consistent u; and the HPS pipeline solution has relerr_res <= 1e-9."""
+    nx = ny = n
+    rng = np.random.default_rng(n * 100 + p)
+    X, Y = P.leaf_coords(nx, ny, p)
+    b = P.crystal_field(X * 0.4 + 0.3, Y * 0.4 + 0.3)
+    f = rng.uniform(-1, 1, X.shape)
+    gb = P.boundary_samples(nx, ny, p, lambda x, y: np.cos(3 * x) + y * y)
+    N, _, _ = O.mesh_info(nx, ny, p)
+    ug = rng.uniform(-1, 1, N)
+    ul = np.stack([ug[O.element_node_index(nx, ny, p, e)] for e in range(nx * ny)])
+    A, rhs, cls = H.assemble_global_dense(nx, ny, p, kappa, b, f, gb)
+    r = A @ ug - rhs
+    with G().LeafStage(p, nx, ny, kappa) as st:
+        res = st.residual(b, f, ul)
+        assert abs(res["r_int2"] - np.sum(r[cls == 0] ** 2)) <= 1e-11 * np.sum(r[cls == 0] ** 2)
+        assert abs(res["r_flux2"] - np.sum(r[cls == 1] ** 2)) <= 1e-11 * np.sum(r[cls == 1] ** 2)
+        assert abs(res["f_int2"] - np.sum(rhs[cls == 0] ** 2)) <= 1e-12 * np.sum(rhs[cls == 0] ** 2)
+        u, parts = H.hps_pipeline(nx, ny, p, kappa, b, f, gb, condense=lambda bb, ff: st.condense(bb, ff)[:2],
+                                  leaf_solve=lambda bb, ff, vv: st.leaf_solve(bb, ff, vv),
+                                  assemble=lambda T, w, g: st.assemble_reduced(T, w, g))
+        res = st.residual(b, f, parts["u_leaf"])
+    g2 = np.sum(rhs[cls == 2] ** 2)
+    relerr_res = math.sqrt((res["r_int2"] + res["r_flux2"]) / (res["f_int2"] + g2))
+    assert relerr_res <= 1e-9, relerr_res
+
+
+def test_residual_full_pipeline_mid_scale():
+    """Eq. 7 relerr_res of the whole pipeline (GPU condense -> GPU scatter -> host SuperLU ->
+    GPU leaf solve) on a 16x16 mesh at p=16 with the crystal field and the Gaussian pulse,
+    evaluated matrix-free on the device."""
+    nx = ny = 16; p = 16; kappa = 40.0
+    X, Y = P.leaf_coords(nx, ny, p)
+    b = P.crystal_field(X, Y); f = np.random.default_rng(2).uniform(-1, 1, X.shape)
+    gb = P.boundary_samples(nx, ny, p, P.gaussian_pulse)
+    with G().LeafStage(p, nx, ny, kappa) as st:
+        _, parts = H.hps_pipeline(nx, ny, p, kappa, b, f, gb, condense=lambda bb, ff: st.condense(bb, ff)[:2],
+                                  leaf_solve=lambda bb, ff, vv: st.leaf_solve(bb, ff, vv),
+                                  assemble=lambda T, w, g: st.assemble_reduced(T, w, g))
+        res = st.residual(b, f, parts["u_leaf"])
+    cls = H.classify(nx, ny, p)
+    Nx = nx * (p - 1) + 1
+    gx, gy = H.global_coords(nx, ny, p)
+    g2 = float(np.sum(P.gaussian_pulse(gx, gy)[cls == 2] ** 2))
+    relerr_res = math.sqrt((res["r_int2"] + res["r_flux2"]) / (res["f_int2"] + g2))
+    assert relerr_res <= 1e-9, relerr_res

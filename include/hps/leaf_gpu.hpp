@@ -126,6 +126,11 @@ class LeafStage {
   std::vector<double> reconstruct_full_solution(const std::vector<double>& u_active,
                                                 const std::vector<double>& f_full = {});
 
+  // Eq. 7 relerr_res = ||A u - f||_2 / ||f||_2 of the full collocation system
+  // (SPEC.md:337-342,354-362 compute_errors) for a full-grid solution u (N values, e.g.
+  // reconstruct_full_solution's output), evaluated matrix-free on the GPU (K6).
+  double relerr_res(const std::vector<double>& u_full, const std::vector<double>& f_full = {});
+
   hps_gpu_ctx* raw() { return ctx_; }
   const MeshTopology& topology() const { return topo_; }
 

@@ -236,6 +236,28 @@ std::vector<double> LeafStage::leaf_solve(int e0, int n, const std::vector<doubl
   return u;
 }
 
+double LeafStage::relerr_res(const std::vector<double>& u_full, const std::vector<double>& f_full) {
+  const int p = topo_.params.p, nx = topo_.params.nx, ny = topo_.params.ny, n = nx * ny;
+  const size_t pp = size_t(p) * p;
+  if (int64_t(u_full.size()) != topo_.N) throw ParameterError("relerr_res: u needs N values");
+  std::vector<double> b, f;
+  sample(0, n, f_full, b, f);
+  std::vector<double> ul(size_t(n) * pp);
+  for_elements(n, cfg_.workers, [&](int e) {
+    const auto gid = topo_.element_node_index(e);
+    for (size_t l = 0; l < pp; ++l) ul[size_t(e) * pp + l] = u_full[gid[l]];
+  });
+  double out[3] = {0.0, 0.0, 0.0};
+  throw_rc(hps_gpu_residual(ctx_, b.data(), f.data(), ul.data(), out), ctx_);
+  // Dirichlet rows (identity, data g) enter ||f|| once per boundary node.
+  const int64_t Nx = int64_t(nx) * (p - 1) + 1, Ny = int64_t(ny) * (p - 1) + 1;
+  const auto g = boundary_samples(topo_, spec_);   // [S(Nx), N(Nx), W(Ny), E(Ny)]
+  double g2 = 0.0;
+  for (int64_t i = 0; i < 2 * Nx; ++i) g2 += g[i] * g[i];
+  for (int64_t i = 1; i < Ny - 1; ++i) g2 += g[2 * Nx + i] * g[2 * Nx + i] + g[2 * Nx + Ny + i] * g[2 * Nx + Ny + i];
+  return std::sqrt((out[0] + out[1]) / (out[2] + g2));
+}
+
 std::vector<double> LeafStage::reconstruct_full_solution(const std::vector<double>& u_active,
                                                          const std::vector<double>& f_full) {
   const int p = topo_.params.p, nx = topo_.params.nx, ny = topo_.params.ny, nb = 4 * (p - 1);

@@ -70,6 +70,9 @@ int main() {
     std::printf("analytic J0 p=%d 4x4: relerr_true %.3e, max corner error %.3e\n", mp.p, rel, cmax);
     if (!(rel <= 1e-6)) { std::printf("FAIL relerr_true\n"); ++fails; }
     if (!(cmax <= 1e-5)) { std::printf("FAIL corner recovery\n"); ++fails; }
+    const double rres = stage.relerr_res(u);   // Eq. 7, matrix-free on the GPU (K6)
+    std::printf("relerr_res %.3e\n", rres);
+    if (!(rres <= 1e-9)) { std::printf("FAIL relerr_res\n"); ++fails; }
     try {
       stage.batched_condense(std::vector<double>(5, 0.0));
       std::printf("FAIL no ParameterError for bad f\n");

@@ -911,6 +911,7 @@ int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b
     }
     cudaEventRecord(ctx->timing_event(3 * slot + 1), st);
     a.d = dsolve;
+    // (lock-step measured no faster for the leaf-solve factorisation: 10.63 vs 10.45 ms at C2)
     hpsg::launch_lu_schur(a, n, st);
     hpsg::launch_backsolve(dsolve, a.ws, a.perm, ctx->in_v[k].as<double>(), ctx->out_u[k].as<double>(),
                            n, st);

@@ -72,6 +72,9 @@ constexpr int NWARP = NT / 32;
 #ifndef HPS_MAX_ROWS
 #define HPS_MAX_ROWS 2048
 #endif
+#ifndef HPS_UNR4_MAXH
+#define HPS_UNR4_MAXH 8
+#endif
 #ifndef HPS_KC
 #define HPS_KC 16
 #endif
@@ -598,7 +601,7 @@ template <int H>
 __device__ void panel_update_t(const Grp& G, const LeafCtx& L, int s0, int d0, int nd, long long* pc,
                                long long& t_phase, double* sbuf) {
   constexpr int NTILE = (H + 7) / 8;        // 8-wide DMMA column tiles (nd <= H)
-  constexpr int UNR = H <= 8 ? 4 : 2;       // 8-row groups in flight per warp
+  constexpr int UNR = H <= HPS_UNR4_MAXH ? 4 : 2;   // 8-row groups in flight per warp
   constexpr int KS = H / 4;                 // DMMA k-steps
   double* Ls = L.scratch;              // H x H   (stride XS)
   double* X = L.scratch + 32 * XS;     // H x 8*NTILE (stride XS), zero padded

@@ -72,6 +72,9 @@ constexpr int NWARP = NT / 32;
 #ifndef HPS_MAX_ROWS
 #define HPS_MAX_ROWS 2048
 #endif
+#ifndef HPS_DIST
+#define HPS_DIST 0   // tile-job prefetch distance in chunks (0: NSTAGE - 1)
+#endif
 #ifndef HPS_UNR4_MAXH
 #define HPS_UNR4_MAXH 8
 #endif
@@ -241,7 +244,10 @@ __device__ void tile_mma(const Grp& G, Acc& acc, const Init& init, const ARow& a
     load_chunk<TL>(pipe + st * TL::STAGE, &full[st], pa, arow, brow, c * KC_, K);
   };
 #pragma unroll
-  for (int s = 0; s < NS_ - 1; ++s)
+  // Prefetch distance DIST <= NS-1 chunks: the refill of chunk c+DIST goes into the stage
+  // of chunk c+DIST-NS, released NS-DIST chunks earlier (slack for slow warps).
+  constexpr int DIST = (HPS_DIST > 0 && HPS_DIST < NS_) ? HPS_DIST : NS_ - 1;
+  for (int s = 0; s < DIST; ++s)
     if (s < nch) fill(s);
   init(acc);   // C-init (load or first-touch assembly) overlaps the prologue copies
   // The refill of the stage freed by chunk c-1 is issued while computing chunk c (before its
@@ -253,11 +259,11 @@ __device__ void tile_mma(const Grp& G, Acc& acc, const Init& init, const ARow& a
     const double* As = pipe + st * TL::STAGE;
     const double* Bs = As + (TL::WM * 32) * TL::LDA;
     if (!act) {
-      if (c + NS_ - 1 < nch) fill(c + NS_ - 1);
+      if (c + DIST < nch) fill(c + DIST);
     } else
 #pragma unroll
     for (int kk = 0; kk < KC_ / 4; ++kk) {
-      if (kk == KC_ / 4 - 1 && c + NS_ - 1 < nch) fill(c + NS_ - 1);
+      if (kk == KC_ / 4 - 1 && c + DIST < nch) fill(c + DIST);
       double a[4], b[4];
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi) a[mi] = sign * As[(32 * wm + 8 * mi + g) * TL::LDA + 4 * kk + t];

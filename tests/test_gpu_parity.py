@@ -414,3 +414,18 @@ def test_residual_full_pipeline_mid_scale():
     g2 = float(np.sum(P.gaussian_pulse(gx, gy)[cls == 2] ** 2))
     relerr_res = math.sqrt((res["r_int2"] + res["r_flux2"]) / (res["f_int2"] + g2))
     assert relerr_res <= 1e-9, relerr_res
+
+
+@pytest.mark.parametrize("p", [16, 22, 32])
+def test_resonance_injection_blocked_kernels(p):
+    """Fault injection through the lock-step (p=16, 22) and persistent 8-warp (p=32) K2
+    kernels: exactly the injected leaves are flagged and the others still match the oracle."""
+    nx, ny = 3, 3
+    b, f = random_leaves(p, nx * ny, seed=p + 1)
+    with G().LeafStage(p, nx, ny, 4.0) as st:
+        st.set_fault_injection([5, 1])
+        T, w, s = st.condense(b, f, raise_on_resonance=False)
+    assert list(np.nonzero(s)[0]) == [1, 5]
+    r = O.batched_condense(p, 1.0 / nx, 4.0, b, f)
+    ok = s == 0
+    assert rel_fro(T[ok], r["T"][ok]).max() <= TOL_T

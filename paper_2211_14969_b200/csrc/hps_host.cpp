@@ -529,7 +529,7 @@ int hps_gpu_create(int device, const hps_leaf_desc* desc, hps_gpu_ctx** out) {
   layout_codes(c->d, false, rows, cols);
   layout_codes(c->ds, true, rows_s, cols_s);
   c->mesh = mesh_tables(D.nx, D.ny, D.p);
-  hps_gpu_ctx* ctxp = c;
+
 #undef CK
 #define CK(call)                                                                        \
   do {                                                                                  \
@@ -538,7 +538,6 @@ int hps_gpu_create(int device, const hps_leaf_desc* desc, hps_gpu_ctx** out) {
       return reject(HPS_ERR_CUDA, std::string(#call) + ": " + cudaGetErrorString(e__)); \
   } while (0)
   {
-    hps_gpu_ctx* ctx = ctxp;  // for CK
     CK(upload(c->Ds, Ds));
     CK(upload(c->D2, D2));
     CK(upload(c->rowcode, rows));
@@ -586,7 +585,6 @@ int hps_gpu_create(int device, const hps_leaf_desc* desc, hps_gpu_ctx** out) {
     return reject(HPS_ERR_PARAM, "ParameterError: device budget below one leaf");
   c->chunk = chunk;
   {
-    hps_gpu_ctx* ctx = ctxp;
     // + 2 rows of slack: 128-wide U tiles may read up to 64 doubles past the last row.
     CK(c->ws.ensure((size_t(chunk) * d.leaf_stride + 2 * size_t(d.ld)) * 8));
     CK(c->linv.ensure(size_t(chunk) * d.nblk * 4096 * 8));

@@ -93,6 +93,18 @@ struct ReducedSystem {
   std::vector<double> rhs;
 };
 
+// The same system as SPEC.md:331's block structure ("(interface edge, interface edge)
+// pairs sharing an element -> dense (p-2)x(p-2) coupling blocks"), in BSR: block row i =
+// interface edge i, bcol_idx = column edges ascending, blocks row-major q x q.
+struct ReducedBlocks {
+  int64_t n_active = 0;
+  int32_t block_size = 0;
+  std::vector<int64_t> brow_ptr;
+  std::vector<int32_t> bcol_idx;
+  std::vector<double> blocks;  // nnzb * q * q
+  std::vector<double> rhs;
+};
+
 namespace b200 {
 
 struct LeafStageConfig {
@@ -116,6 +128,8 @@ class LeafStage {
   std::vector<CondensedLeaf> batched_condense(const std::vector<double>& f_full = {});
   // assemble_reduced(topo, leaves, spec).
   ReducedSystem assemble_reduced(const std::vector<CondensedLeaf>& leaves);
+  // assemble_reduced in the BSR block view (entries bit-identical to the CSR values).
+  ReducedBlocks assemble_reduced_blocks(const std::vector<CondensedLeaf>& leaves);
   // Batched leaf_solve: boundary values v (n_b per element, SPEC boundary order)
   // for elements [e0, e0 + n) -> p*p local values each.
   std::vector<double> leaf_solve(int e0, int n, const std::vector<double>& v,

@@ -147,6 +147,21 @@ int hps_gpu_assemble_reduced_device(hps_gpu_ctx* ctx, const double* d_T, const d
                                     const double* d_g_bnd, double* d_values, double* d_rhs,
                                     void* stream);
 
+/* BSR view of the same reduced system (ReducedSystem.blocks maps
+ * (interface edge, interface edge) pairs sharing an element to dense (p-2)x(p-2)
+ * coupling blocks).  Block row i = interface edge i (active rows
+ * i*q .. i*q+q-1, q = p-2 = *block_size), int64 brow_ptr (n_active/q + 1), int32
+ * bcol_idx (nnzb, block columns = edge ids, ascending); call with brow_ptr == NULL
+ * for block_size and nnzb only.  Values: nnzb blocks of q*q, row-major, holding
+ * bit-for-bit the entries hps_gpu_assemble_reduced puts in CSR; rhs identical. */
+int hps_gpu_reduced_bsr_pattern(hps_gpu_ctx* ctx, int32_t* block_size, int64_t* nnzb,
+                                int64_t* brow_ptr, int32_t* bcol_idx);
+int hps_gpu_assemble_reduced_bsr(hps_gpu_ctx* ctx, const double* T, const double* w,
+                                 const double* g_bnd, double* bvalues, double* rhs);
+int hps_gpu_assemble_reduced_bsr_device(hps_gpu_ctx* ctx, const double* d_T, const double* d_w,
+                                        const double* d_g_bnd, double* d_bvalues, double* d_rhs,
+                                        void* stream);
+
 /* Test hook: zero interior row 0 of A_ii for these element
  * ids, which forces a zero pivot.  n = 0 clears. */
 int hps_gpu_set_fault_injection(hps_gpu_ctx* ctx, const int32_t* elements, int32_t n);

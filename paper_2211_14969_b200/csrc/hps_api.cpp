@@ -198,17 +198,25 @@ static std::vector<double> boundary_samples(const MeshTopology& t, const Problem
   return g;
 }
 
-ReducedSystem LeafStage::assemble_reduced(const std::vector<CondensedLeaf>& leaves) {
-  const int n = topo_.params.nx * topo_.params.ny;
-  const int nb = 4 * (topo_.params.p - 1);
+// Gathers the leaves' T and w leaf-major (SPEC.md:349's ordering guard).
+static void gather_leaves(const MeshTopology& topo, const std::vector<CondensedLeaf>& leaves,
+                          std::vector<double>& T, std::vector<double>& w) {
+  const int n = topo.params.nx * topo.params.ny;
+  const int nb = 4 * (topo.params.p - 1);
   if (int(leaves.size()) != n) throw ParameterError("assemble_reduced: one condensed leaf per element");
-  std::vector<double> T(size_t(n) * nb * nb), w(size_t(n) * nb);
+  T.resize(size_t(n) * nb * nb);
+  w.resize(size_t(n) * nb);
   for (int e = 0; e < n; ++e) {
     if (leaves[e].element_id != e || int(leaves[e].T_flux.size()) != nb * nb)
       throw ParameterError("assemble_reduced: inconsistent leaf ordering");
     std::copy(leaves[e].T_flux.begin(), leaves[e].T_flux.end(), T.begin() + size_t(e) * nb * nb);
     std::copy(leaves[e].w_equiv.begin(), leaves[e].w_equiv.end(), w.begin() + size_t(e) * nb);
   }
+}
+
+ReducedSystem LeafStage::assemble_reduced(const std::vector<CondensedLeaf>& leaves) {
+  std::vector<double> T, w;
+  gather_leaves(topo_, leaves, T, w);
   ReducedSystem r;
   r.n_active = topo_.n_active;
   int64_t nnz = 0;
@@ -220,6 +228,26 @@ ReducedSystem LeafStage::assemble_reduced(const std::vector<CondensedLeaf>& leav
   throw_rc(hps_gpu_reduced_pattern(ctx_, &nnz, r.row_ptr.data(), r.col_idx.data()), ctx_);
   const auto g = boundary_samples(topo_, spec_);
   throw_rc(hps_gpu_assemble_reduced(ctx_, T.data(), w.data(), g.data(), r.values.data(), r.rhs.data()),
+           ctx_);
+  return r;
+}
+
+ReducedBlocks LeafStage::assemble_reduced_blocks(const std::vector<CondensedLeaf>& leaves) {
+  std::vector<double> T, w;
+  gather_leaves(topo_, leaves, T, w);
+  ReducedBlocks r;
+  r.n_active = topo_.n_active;
+  int64_t nnzb = 0;
+  throw_rc(hps_gpu_reduced_bsr_pattern(ctx_, &r.block_size, &nnzb, nullptr, nullptr), ctx_);
+  const int64_t q = r.block_size;
+  r.brow_ptr.resize(size_t(q > 0 ? r.n_active / q : 0) + 1);
+  r.bcol_idx.resize(size_t(nnzb));
+  r.blocks.resize(size_t(nnzb * q * q));
+  r.rhs.resize(size_t(r.n_active));
+  throw_rc(hps_gpu_reduced_bsr_pattern(ctx_, &r.block_size, &nnzb, r.brow_ptr.data(), r.bcol_idx.data()),
+           ctx_);
+  const auto g = boundary_samples(topo_, spec_);
+  throw_rc(hps_gpu_assemble_reduced_bsr(ctx_, T.data(), w.data(), g.data(), r.blocks.data(), r.rhs.data()),
            ctx_);
   return r;
 }

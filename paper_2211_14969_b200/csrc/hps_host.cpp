@@ -954,19 +954,56 @@ int hps_gpu_reduced_pattern(hps_gpu_ctx* ctx, int64_t* nnz, int64_t* row_ptr, in
   return HPS_OK;
 }
 
-int hps_gpu_assemble_reduced_device(hps_gpu_ctx* ctx, const double* d_T, const double* d_w,
-                                    const double* d_g_bnd, double* d_values, double* d_rhs,
-                                    void* stream) {
+int hps_gpu_reduced_bsr_pattern(hps_gpu_ctx* ctx, int32_t* block_size, int64_t* nnzb,
+                                int64_t* brow_ptr, int32_t* bcol_idx) {
+  if (!ctx || !block_size || !nnzb) return HPS_ERR_PARAM;
+  const int64_t q = ctx->d.p - 2;
+  *block_size = int32_t(q);
+  *nnzb = ctx->mesh.nnz / (q * q);
+  if (!brow_ptr) return HPS_OK;
+  if (!bcol_idx) return ctx->fail(HPS_ERR_PARAM, "ParameterError: null bcol_idx");
+  CK(cudaSetDevice(ctx->device));
+  const int64_t nbr = ctx->mesh.n_active / q;
+  if (nbr == 0) {
+    brow_ptr[0] = 0;
+    return HPS_OK;
+  }
+  DevBuf rp, ci;
+  CK(rp.ensure(size_t(nbr + 1) * 8));
+  CK(ci.ensure(size_t(std::max<int64_t>(1, *nnzb)) * 4));
+  hpsg::launch_reduced_bsr_pattern(ctx->mesh_dev(), rp.as<int64_t>(), ci.as<int32_t>(), ctx->s_comp);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(brow_ptr, rp.ptr, size_t(nbr + 1) * 8, cudaMemcpyDeviceToHost, ctx->s_comp));
+  CK(cudaMemcpyAsync(bcol_idx, ci.ptr, size_t(*nnzb) * 4, cudaMemcpyDeviceToHost, ctx->s_comp));
+  CK(cudaStreamSynchronize(ctx->s_comp));
+  return HPS_OK;
+}
+
+static int assemble_reduced_device(hps_gpu_ctx* ctx, const double* d_T, const double* d_w,
+                                   const double* d_g_bnd, double* d_values, double* d_rhs,
+                                   void* stream, bool bsr) {
   if (!ctx) return HPS_ERR_PARAM;
   CK(cudaSetDevice(ctx->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->s_comp;
-  hpsg::launch_reduced_values(ctx->mesh_dev(), d_T, d_w, d_g_bnd, d_values, d_rhs, st);
+  hpsg::launch_reduced_values(ctx->mesh_dev(), d_T, d_w, d_g_bnd, d_values, d_rhs, st, bsr);
   CK(cudaGetLastError());
   return HPS_OK;
 }
 
-int hps_gpu_assemble_reduced(hps_gpu_ctx* ctx, const double* T, const double* w,
-                             const double* g_bnd, double* values, double* rhs) {
+int hps_gpu_assemble_reduced_device(hps_gpu_ctx* ctx, const double* d_T, const double* d_w,
+                                    const double* d_g_bnd, double* d_values, double* d_rhs,
+                                    void* stream) {
+  return assemble_reduced_device(ctx, d_T, d_w, d_g_bnd, d_values, d_rhs, stream, false);
+}
+
+int hps_gpu_assemble_reduced_bsr_device(hps_gpu_ctx* ctx, const double* d_T, const double* d_w,
+                                        const double* d_g_bnd, double* d_bvalues, double* d_rhs,
+                                        void* stream) {
+  return assemble_reduced_device(ctx, d_T, d_w, d_g_bnd, d_bvalues, d_rhs, stream, true);
+}
+
+static int assemble_reduced_host(hps_gpu_ctx* ctx, const double* T, const double* w,
+                                 const double* g_bnd, double* values, double* rhs, bool bsr) {
   if (!ctx || !T || !w || !g_bnd || !values || !rhs) return HPS_ERR_PARAM;
   CK(cudaSetDevice(ctx->device));
   const LeafDims& d = ctx->d;
@@ -990,7 +1027,7 @@ int hps_gpu_assemble_reduced(hps_gpu_ctx* ctx, const double* T, const double* w,
   CK(cudaEventCreate(&t1));
   cudaEventRecord(t0, st);
   hpsg::launch_reduced_values(ctx->mesh_dev(), dT.as<double>(), dw.as<double>(), dg.as<double>(),
-                              dv.as<double>(), dr.as<double>(), st);
+                              dv.as<double>(), dr.as<double>(), st, bsr);
   cudaEventRecord(t1, st);
   CK(cudaGetLastError());
   CK(cudaMemcpyAsync(values, dv.ptr, size_t(nnz) * 8, cudaMemcpyDeviceToHost, st));
@@ -1002,6 +1039,16 @@ int hps_gpu_assemble_reduced(hps_gpu_ctx* ctx, const double* T, const double* w,
   ctx->tkernels = 1;
   finish_timing(ctx);
   return HPS_OK;
+}
+
+int hps_gpu_assemble_reduced(hps_gpu_ctx* ctx, const double* T, const double* w,
+                             const double* g_bnd, double* values, double* rhs) {
+  return assemble_reduced_host(ctx, T, w, g_bnd, values, rhs, false);
+}
+
+int hps_gpu_assemble_reduced_bsr(hps_gpu_ctx* ctx, const double* T, const double* w,
+                                 const double* g_bnd, double* bvalues, double* rhs) {
+  return assemble_reduced_host(ctx, T, w, g_bnd, bvalues, rhs, true);
 }
 
 }  // extern "C"

@@ -136,8 +136,10 @@ struct MeshDev {
   const int64_t* edge_off; // first nonzero of the edge's rows
 };
 void launch_reduced_pattern(const MeshDev& m, int64_t* row_ptr, int32_t* col_idx, cudaStream_t st);
+// bsr: values in BSR layout (block row = interface edge, q x q row-major blocks).
 void launch_reduced_values(const MeshDev& m, const double* T, const double* w, const double* g_bnd,
-                           double* values, double* rhs, cudaStream_t st);
+                           double* values, double* rhs, cudaStream_t st, bool bsr = false);
+void launch_reduced_bsr_pattern(const MeshDev& m, int64_t* brow_ptr, int32_t* bcol_idx, cudaStream_t st);
 
 // K6: matrix-free residual of the global collocation system (k6_residual.cu): per-leaf
 // [sum r_int^2, sum f_int^2] into part_leaf (2 per leaf), per-edge sum r_flux^2 into

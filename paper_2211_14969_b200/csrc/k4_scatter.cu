@@ -13,6 +13,14 @@
 //  in exactly the order of the CPU oracle, with _rn intrinsics (no FMA
 //  contraction): given the same T, values and rhs are bit-identical.
 //  HBM bound: reads the active x active part of T, writes nnz values.
+//
+//  BSR view (SPEC.md:331's ReducedSystem "blocks" are exactly
+//  this): block row = interface edge, block column = one of its <= 7 column
+//  edges (ascending), block = the dense q x q coupling, row-major.  Since every
+//  row of an edge has the same columns, block (ed, rank) holds the entries
+//  CSR keeps at edge_off[ed] + k*rowlen + rank*q + kk; the BSR kernel writes
+//  them at edge_off[ed] + rank*q*q + k*q + kk (same values, same bits), and
+//  block offsets are edge_off[ed] / (q*q) + rank.
 // ============================================================================
 #include "hps_device.cuh"
 #include "hps_kernels.h"
@@ -43,7 +51,22 @@ __global__ void __launch_bounds__(256) k4_pattern_kernel(MeshDev m, int64_t* __r
   }
 }
 
-// grid = n_edges, block 256
+// grid = n_edges, block 256.  BSR: block row pointer (n_edges + 1) and block columns.
+__global__ void __launch_bounds__(256) k4_bsr_pattern_kernel(MeshDev m, int64_t* __restrict__ brow_ptr,
+                                                             int32_t* __restrict__ bcol_idx) {
+  const int ed = blockIdx.x;
+  const int q = m.p - 2;
+  const int ne = m.edge_ne[ed];
+  const int64_t boff = m.edge_off[ed] / ((int64_t)q * q);
+  if (threadIdx.x == 0) {
+    brow_ptr[ed] = boff;
+    if (ed == m.n_edges - 1) brow_ptr[ed + 1] = boff + ne;
+  }
+  if (threadIdx.x < ne) bcol_idx[boff + threadIdx.x] = m.edge_cols[ed * 7 + threadIdx.x];
+}
+
+// grid = n_edges, block 256.  BSR selects the output layout (see the header).
+template <bool BSR>
 __global__ void __launch_bounds__(256) k4_values_kernel(MeshDev m, const double* __restrict__ T,
                                                         const double* __restrict__ w,
                                                         const double* __restrict__ g_bnd,
@@ -83,8 +106,18 @@ __global__ void __launch_bounds__(256) k4_values_kernel(MeshDev m, const double*
       has[u][0] = has[u][1] = false;
       tv[u][0] = tv[u][1] = 0.0;
       if (e < total) {
-        const int k = e / rowlen, pos = e - k * rowlen;
-        const int rank = pos / q, kk = pos - rank * q;
+        int k, rank, kk;
+        if (BSR) {
+          rank = e / (q * q);
+          const int rem = e - rank * q * q;
+          k = rem / q;
+          kk = rem - k * q;
+        } else {
+          k = e / rowlen;
+          const int pos = e - k * rowlen;
+          rank = pos / q;
+          kk = pos - rank * q;
+        }
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
           const int sc = col_side[t][rank];
@@ -142,10 +175,18 @@ void launch_reduced_pattern(const MeshDev& m, int64_t* row_ptr, int32_t* col_idx
   k4_pattern_kernel<<<m.n_edges, 256, 0, st>>>(m, row_ptr, col_idx);
 }
 
-void launch_reduced_values(const MeshDev& m, const double* T, const double* w, const double* g_bnd,
-                           double* values, double* rhs, cudaStream_t st) {
+void launch_reduced_bsr_pattern(const MeshDev& m, int64_t* brow_ptr, int32_t* bcol_idx, cudaStream_t st) {
   if (m.n_edges <= 0) return;
-  k4_values_kernel<<<m.n_edges, 256, 0, st>>>(m, T, w, g_bnd, values, rhs);
+  k4_bsr_pattern_kernel<<<m.n_edges, 256, 0, st>>>(m, brow_ptr, bcol_idx);
+}
+
+void launch_reduced_values(const MeshDev& m, const double* T, const double* w, const double* g_bnd,
+                           double* values, double* rhs, cudaStream_t st, bool bsr) {
+  if (m.n_edges <= 0) return;
+  if (bsr)
+    k4_values_kernel<true><<<m.n_edges, 256, 0, st>>>(m, T, w, g_bnd, values, rhs);
+  else
+    k4_values_kernel<false><<<m.n_edges, 256, 0, st>>>(m, T, w, g_bnd, values, rhs);
 }
 
 }  // namespace hpsg

@@ -59,7 +59,9 @@ EXPORTED = ["hps_gpu_create", "hps_gpu_destroy", "hps_gpu_last_error", "hps_gpu_
             "hps_gpu_get_timing", "hps_gpu_reset_timing", "hps_gpu_condense", "hps_gpu_condense_device", "hps_gpu_leaf_solve",
             "hps_gpu_reduced_pattern", "hps_gpu_assemble_reduced", "hps_gpu_assemble_reduced_device",
             "hps_gpu_set_fault_injection", "hps_host_alloc", "hps_host_free", "hps_gpu_version",
-            "hps_gpu_sample_crystal", "hps_gpu_residual", "hps_gpu_residual_device"]
+            "hps_gpu_sample_crystal", "hps_gpu_residual", "hps_gpu_residual_device",
+            "hps_gpu_reduced_bsr_pattern", "hps_gpu_assemble_reduced_bsr",
+            "hps_gpu_assemble_reduced_bsr_device"]
 
 
 def lib():
@@ -81,7 +83,9 @@ def lib():
                      "hps_gpu_reduced_pattern", "hps_gpu_assemble_reduced",
                      "hps_gpu_assemble_reduced_device", "hps_gpu_set_fault_injection",
                      "hps_gpu_get_info", "hps_gpu_get_timing", "hps_gpu_reset_timing",
-                     "hps_gpu_sample_crystal", "hps_gpu_residual", "hps_gpu_residual_device"):
+                     "hps_gpu_sample_crystal", "hps_gpu_residual", "hps_gpu_residual_device",
+                     "hps_gpu_reduced_bsr_pattern", "hps_gpu_assemble_reduced_bsr",
+                     "hps_gpu_assemble_reduced_bsr_device"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -231,6 +235,25 @@ class LeafStage:
         T = _f64(T); w = _f64(w); g_bnd = _f64(g_bnd)
         vals = np.empty(ci.size); rhs = np.empty(rp.size - 1)
         self._check(lib().hps_gpu_assemble_reduced(self._h, _ptr(T), _ptr(w), _ptr(g_bnd), _ptr(vals), _ptr(rhs)))
+        return rp, ci, vals, rhs
+
+    def reduced_bsr_pattern(self):
+        """BSR pattern of the reduced system (SPEC.md:331 ReducedSystem.blocks): block row =
+        interface edge, q x q blocks, q = p-2. Returns (q, brow_ptr, bcol_idx)."""
+        q = C.c_int32(); nnzb = C.c_int64()
+        self._check(lib().hps_gpu_reduced_bsr_pattern(self._h, C.byref(q), C.byref(nnzb), None, None))
+        nbr = self.info()["n_active"] // max(q.value, 1)
+        rp = np.empty(nbr + 1, np.int64); ci = np.empty(max(nnzb.value, 1), np.int32)
+        self._check(lib().hps_gpu_reduced_bsr_pattern(self._h, C.byref(q), C.byref(nnzb), _ptr(rp), _ptr(ci)))
+        return q.value, rp, ci[:nnzb.value]
+
+    def assemble_reduced_bsr(self, T, w, g_bnd):
+        """assemble_reduced in BSR: (brow_ptr, bcol_idx, blocks[nnzb, q, q], rhs); the entries
+        are bit-identical to assemble_reduced's CSR values."""
+        q, rp, ci = self.reduced_bsr_pattern()
+        T = _f64(T); w = _f64(w); g_bnd = _f64(g_bnd)
+        vals = np.empty((ci.size, q, q)); rhs = np.empty((rp.size - 1) * q)
+        self._check(lib().hps_gpu_assemble_reduced_bsr(self._h, _ptr(T), _ptr(w), _ptr(g_bnd), _ptr(vals), _ptr(rhs)))
         return rp, ci, vals, rhs
 
 

@@ -50,6 +50,25 @@ int main() {
     hps::b200::LeafStage stage(topo, spec);
     const auto leaves = stage.batched_condense();
     const auto red = stage.assemble_reduced(leaves);
+    {  // BSR view (SPEC.md:331 blocks): every block entry equals its CSR entry bit for bit
+      const auto blk = stage.assemble_reduced_blocks(leaves);
+      const int64_t q = blk.block_size;
+      int64_t bad = (q != mp.p - 2) || (blk.rhs != red.rhs) ? 1 : 0;
+      for (int64_t br = 0; br + 1 < int64_t(blk.brow_ptr.size()); ++br)
+        for (int64_t b = blk.brow_ptr[br]; b < blk.brow_ptr[br + 1]; ++b)
+          for (int64_t k = 0; k < q; ++k) {
+            const int64_t row = br * q + k, rank = b - blk.brow_ptr[br];
+            const int64_t rowlen = (blk.brow_ptr[br + 1] - blk.brow_ptr[br]) * q;
+            for (int64_t kk = 0; kk < q; ++kk) {
+              const int64_t c = red.row_ptr[row] + rank * q + kk;
+              bad += red.col_idx[c] != blk.bcol_idx[b] * q + kk;
+              bad += red.values[c] != blk.blocks[(b * q + k) * q + kk];
+            }
+            bad += red.row_ptr[row + 1] - red.row_ptr[row] != rowlen;
+          }
+      std::printf("BSR view: %zu blocks, mismatches %lld\n", blk.bcol_idx.size(), (long long)bad);
+      if (bad) { std::printf("FAIL BSR view\n"); ++fails; }
+    }
     const auto ua = dense_solve(int(red.n_active), red);
     const auto u = stage.reconstruct_full_solution(ua);
     const int64_t Nx = mp.nx * (mp.p - 1) + 1;

@@ -112,6 +112,52 @@ def test_reduced_values_bit_exact_given_T(nx, ny, p):
     assert np.array_equal(r.view(np.int64), ro.view(np.int64))
 
 
+def oracle_bsr(nx, ny, p, rp, ci, vals):
+    """BSR view of the oracle's CSR (SPEC.md:331 ReducedSystem.blocks): block row = interface
+    edge (q = p-2 rows), block columns = the distinct column edges of its rows, q x q blocks."""
+    q = p - 2
+    nbr = (rp.size - 1) // q
+    brp = [0]; bci = []; blocks = []
+    for br in range(nbr):
+        lo, hi = rp[br * q], rp[br * q + q]
+        ne = (rp[br * q + 1] - lo) // q
+        cols = ci[lo:hi].reshape(q, ne, q)
+        v = vals[lo:hi].reshape(q, ne, q)
+        assert (cols == cols[0]).all()                     # every row of the edge shares columns
+        assert (cols[0] // q == cols[0, :, :1] // q).all() and (cols[0] % q == np.arange(q)).all()
+        bci += list(cols[0, :, 0] // q)
+        blocks.append(v.transpose(1, 0, 2))
+        brp.append(brp[-1] + ne)
+    return (np.array(brp, np.int64), np.array(bci, np.int32),
+            np.concatenate(blocks) if blocks else np.zeros((0, q, q)))
+
+
+@pytest.mark.parametrize("nx,ny,p", [(2, 2, 4), (2, 2, 8), (3, 5, 10), (6, 4, 12), (5, 3, 22), (4, 4, 42)])
+def test_reduced_bsr_view_bit_exact(nx, ny, p):
+    """BSR view: pattern equal to the oracle CSR regrouped by edge blocks, block
+    entries bit-identical to the oracle's CSR values, rhs identical, and the BSR matrix equals
+    the CSR matrix."""
+    import scipy.sparse as sp
+    rng = np.random.default_rng(12)
+    nb = 4 * (p - 1)
+    T = rng.standard_normal((nx * ny, nb, nb)); w = rng.standard_normal((nx * ny, nb))
+    gb = P.boundary_samples(nx, ny, p, lambda x, y: np.sin(2 * x) - y)
+    rpo, cio, vo, ro = O.assemble_reduced(nx, ny, p, T, w, gb)
+    ebrp, ebci, eblk = oracle_bsr(nx, ny, p, rpo, cio, vo)
+    with G().LeafStage(p, nx, ny, 1.0) as st:
+        q, brp, bci = st.reduced_bsr_pattern()
+        brp2, bci2, blk, r = st.assemble_reduced_bsr(T, w, gb)
+    assert q == p - 2
+    assert brp.dtype == np.int64 and bci.dtype == np.int32
+    assert np.array_equal(brp, ebrp) and np.array_equal(bci, ebci)
+    assert np.array_equal(brp2, brp) and np.array_equal(bci2, bci)
+    assert np.array_equal(blk.view(np.int64), eblk.view(np.int64))
+    assert np.array_equal(r.view(np.int64), ro.view(np.int64))
+    A_bsr = sp.bsr_matrix((blk, bci, brp), shape=(ro.size, ro.size)).tocsr()
+    A_csr = sp.csr_matrix((vo, cio, rpo), shape=(ro.size, ro.size))
+    assert (A_bsr != A_csr).nnz == 0
+
+
 @pytest.mark.parametrize("p,kappa", [(8, 5.0), (12, 20.0), (22, 100.0), (27, 60.0)])
 def test_leaf_solve_parity_and_store_equals_recompute(p, kappa):
     n = 5

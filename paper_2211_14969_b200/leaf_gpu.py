@@ -279,3 +279,26 @@ class PinnedArray:
             self.free()
         except Exception:
             pass
+
+
+def write_reduced_coo(path, row_ptr, col_idx, values, rhs=None):
+    """Coordinate-triplet dump of the reduced system for external solver debugging
+    (SPEC.md assembly module, "External Interfaces: optional dump of the reduced system in
+    coordinate-triplet text format").  Writes Matrix Market `coordinate real general`
+    (1-based i j value, %.17g so every double round-trips bit for bit) to `path`, and the
+    rhs, when given, as a Matrix Market `array` to `path + ".rhs"`.  Host-side plumbing
+    over the CSR that assemble_reduced returns; nothing here touches the GPU."""
+    row_ptr = np.asarray(row_ptr, np.int64)
+    n = row_ptr.size - 1
+    rows = np.repeat(np.arange(1, n + 1, dtype=np.int64), np.diff(row_ptr))
+    cols = np.asarray(col_idx, np.int64) + 1
+    with open(path, "w") as fh:
+        fh.write("%%MatrixMarket matrix coordinate real general\n")
+        fh.write(f"{n} {n} {rows.size}\n")
+        np.savetxt(fh, np.column_stack([rows, cols, np.asarray(values, np.float64)]),
+                   fmt=["%d", "%d", "%.17g"])
+    if rhs is not None:
+        with open(str(path) + ".rhs", "w") as fh:
+            fh.write("%%MatrixMarket matrix array real general\n")
+            fh.write(f"{n} 1\n")
+            np.savetxt(fh, np.asarray(rhs, np.float64), fmt="%.17g")

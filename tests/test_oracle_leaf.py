@@ -244,3 +244,27 @@ def test_true_accuracy_p16():
     ue = ut(GX, GY)
     rel = np.linalg.norm(u[m] - ue[m]) / np.linalg.norm(ue[m])
     assert rel <= 1e-6, rel
+
+
+def test_reduced_coo_triplet_dump_roundtrip(tmp_path):
+    """SPEC assembly 'External Interfaces': the coordinate-triplet dump of the reduced system
+    reads back (scipy Matrix Market reader) as the same matrix and rhs, bit for bit."""
+    import scipy.io
+    import scipy.sparse as sp
+    from paper_2211_14969_b200.leaf_gpu import write_reduced_coo
+    nx, ny, p = 3, 2, 6
+    rng = np.random.default_rng(5)
+    nb = 4 * (p - 1)
+    T = rng.standard_normal((nx * ny, nb, nb)); w = rng.standard_normal((nx * ny, nb))
+    gb = P.boundary_samples(nx, ny, p, lambda x, y: x - 2 * y)
+    rp, ci, v, r = O.assemble_reduced(nx, ny, p, T, w, gb)
+    path = tmp_path / "reduced.mtx"
+    write_reduced_coo(str(path), rp, ci, v, r)
+    A = scipy.io.mmread(str(path)).tocsr()
+    A.sort_indices()
+    ref = sp.csr_matrix((v, ci, rp), shape=(r.size, r.size))
+    assert A.shape == ref.shape and A.nnz == ref.nnz
+    assert np.array_equal(A.indptr, ref.indptr) and np.array_equal(A.indices, ref.indices)
+    assert np.array_equal(A.data.view(np.int64), ref.data.view(np.int64))
+    rr = np.asarray(scipy.io.mmread(str(path) + ".rhs")).ravel()
+    assert np.array_equal(rr.view(np.int64), r.view(np.int64))

@@ -137,6 +137,15 @@ int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b
  * over active nodes, int64 row_ptr (n_active+1), int32 col_idx
  * (nnz).  Call with row_ptr == NULL to get nnz only. */
 int hps_gpu_reduced_pattern(hps_gpu_ctx* ctx, int64_t* nnz, int64_t* row_ptr, int32_t* col_idx);
+/* Per-leaf scatter map of assemble_reduced (SURVEY.md §8b hps_gpu_scatter_indices; the
+ * COO/CSR indexing of SPEC.md:345-353,382), leaves [e0, e1), caller-owned host buffers:
+ *   row[(e-e0)*nb + r]            active row of local boundary node r, -1 if corner/Dirichlet;
+ *   slot[((e-e0)*nb + r)*nb + c]  index into the CSR values of hps_gpu_reduced_pattern that
+ *                                 T_e[r, c] is summed into, -1 if row or column is inactive.
+ * nb = 4(p-1); local boundary order S, E, N, W.  Bit-exact with
+ * the CPU oracle's pattern; values[slot] accumulated in ascending e reproduce
+ * hps_gpu_assemble_reduced's values bit for bit. */
+int hps_gpu_scatter_indices(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, int64_t* slot, int64_t* row);
 /* Values/rhs from all leaves' T and w (host, leaf-major, all nx*ny leaves) and
  * Dirichlet samples g_bnd = [south(Nx) | north(Nx) | west(Ny) | east(Ny)],
  * Nx = nx(p-1)+1, Ny = ny(p-1)+1. */

@@ -954,6 +954,25 @@ int hps_gpu_reduced_pattern(hps_gpu_ctx* ctx, int64_t* nnz, int64_t* row_ptr, in
   return HPS_OK;
 }
 
+int hps_gpu_scatter_indices(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, int64_t* slot, int64_t* row) {
+  if (!ctx) return HPS_ERR_PARAM;
+  if (e0 < 0 || e1 < e0 || e1 > ctx->n_leaves)
+    return ctx->fail(HPS_ERR_PARAM, "ParameterError: element range out of bounds");
+  if (e1 == e0) return HPS_OK;
+  if (!slot || !row) return ctx->fail(HPS_ERR_PARAM, "ParameterError: null output");
+  CK(cudaSetDevice(ctx->device));
+  const int64_t n = e1 - e0, nb = 4 * (ctx->d.p - 1);
+  DevBuf ds, dr;
+  CK(ds.ensure(size_t(n * nb * nb) * 8));
+  CK(dr.ensure(size_t(n * nb) * 8));
+  hpsg::launch_scatter_indices(ctx->mesh_dev(), e0, int(n), ds.as<int64_t>(), dr.as<int64_t>(), ctx->s_comp);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(slot, ds.ptr, size_t(n * nb * nb) * 8, cudaMemcpyDeviceToHost, ctx->s_comp));
+  CK(cudaMemcpyAsync(row, dr.ptr, size_t(n * nb) * 8, cudaMemcpyDeviceToHost, ctx->s_comp));
+  CK(cudaStreamSynchronize(ctx->s_comp));
+  return HPS_OK;
+}
+
 int hps_gpu_reduced_bsr_pattern(hps_gpu_ctx* ctx, int32_t* block_size, int64_t* nnzb,
                                 int64_t* brow_ptr, int32_t* bcol_idx) {
   if (!ctx || !block_size || !nnzb) return HPS_ERR_PARAM;

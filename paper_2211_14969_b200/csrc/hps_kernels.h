@@ -140,6 +140,8 @@ void launch_reduced_pattern(const MeshDev& m, int64_t* row_ptr, int32_t* col_idx
 void launch_reduced_values(const MeshDev& m, const double* T, const double* w, const double* g_bnd,
                            double* values, double* rhs, cudaStream_t st, bool bsr = false);
 void launch_reduced_bsr_pattern(const MeshDev& m, int64_t* brow_ptr, int32_t* bcol_idx, cudaStream_t st);
+// Per-leaf scatter map for leaves [e0, e0+n): slot (n x nb x nb) into the CSR values, row (n x nb).
+void launch_scatter_indices(const MeshDev& m, int e0, int n, int64_t* slot, int64_t* row, cudaStream_t st);
 
 // K6: matrix-free residual of the global collocation system (k6_residual.cu): per-leaf
 // [sum r_int^2, sum f_int^2] into part_leaf (2 per leaf), per-edge sum r_flux^2 into

@@ -170,6 +170,60 @@ __global__ void __launch_bounds__(256) k4_values_kernel(MeshDev m, const double*
   }
 }
 
+// Per-leaf scatter map (the COO view of the same CSR; SURVEY §8b hps_gpu_scatter_indices):
+// for leaf e and local boundary index r (SURVEY A.4 order) row[e][r] = active row of that
+// node or -1 (corner / Dirichlet); slot[e][r][c] = position in the CSR values array that
+// T_e[r, c] is summed into, or -1 when the row or the column is not active (Gamma columns go
+// to the rhs).  grid = leaves, block 256.
+__global__ void __launch_bounds__(256) k4_scatter_index_kernel(MeshDev m, int e0, int64_t* __restrict__ slot,
+                                                               int64_t* __restrict__ row) {
+  const int le = blockIdx.x, e = e0 + le;
+  const int p = m.p, q = p - 2, nb = 4 * (p - 1);
+  __shared__ int r_edge[4 * 64], r_k[4 * 64];   // per local boundary index (nb <= 4*63)
+  __shared__ int rank_of[4][4];                   // [row side][col side] -> column rank, -1 if absent
+  for (int r = threadIdx.x; r < nb; r += blockDim.x) {
+    int ed = -1, k = -1;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int kk = r - side_base(p, s);
+      if (kk >= 0 && kk < q) {
+        ed = m.elem_edges[4 * e + s];
+        k = kk;
+      }
+    }
+    r_edge[r] = ed;
+    r_k[r] = ed >= 0 ? k : -1;
+    row[(size_t)le * nb + r] = ed >= 0 ? (int64_t)ed * q + k : -1;
+  }
+  if (threadIdx.x < 16) {
+    const int sr = threadIdx.x / 4, sc = threadIdx.x % 4;
+    const int er = m.elem_edges[4 * e + sr], ec = m.elem_edges[4 * e + sc];
+    int rk = -1;
+    if (er >= 0 && ec >= 0)
+      for (int t = 0; t < m.edge_ne[er]; ++t)
+        if (m.edge_cols[er * 7 + t] == ec) rk = t;
+    rank_of[sr][sc] = rk;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nb * nb; i += blockDim.x) {
+    const int r = i / nb, c = i - r * nb;
+    int64_t out = -1;
+    const int er = r_edge[r], ec = r_edge[c];
+    if (er >= 0 && ec >= 0) {
+      int sr = 0, sc = 0;
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        if (m.elem_edges[4 * e + s] == er) sr = s;
+        if (m.elem_edges[4 * e + s] == ec) sc = s;
+      }
+      const int rk = rank_of[sr][sc];
+      const int rowlen = m.edge_ne[er] * q;
+      out = m.edge_off[er] + (int64_t)r_k[r] * rowlen + (int64_t)rk * q + r_k[c];
+    }
+    slot[(size_t)le * nb * nb + i] = out;
+  }
+}
+
 void launch_reduced_pattern(const MeshDev& m, int64_t* row_ptr, int32_t* col_idx, cudaStream_t st) {
   if (m.n_edges <= 0) return;
   k4_pattern_kernel<<<m.n_edges, 256, 0, st>>>(m, row_ptr, col_idx);
@@ -187,6 +241,11 @@ void launch_reduced_values(const MeshDev& m, const double* T, const double* w, c
     k4_values_kernel<true><<<m.n_edges, 256, 0, st>>>(m, T, w, g_bnd, values, rhs);
   else
     k4_values_kernel<false><<<m.n_edges, 256, 0, st>>>(m, T, w, g_bnd, values, rhs);
+}
+
+void launch_scatter_indices(const MeshDev& m, int e0, int n, int64_t* slot, int64_t* row, cudaStream_t st) {
+  if (n <= 0) return;
+  k4_scatter_index_kernel<<<n, 256, 0, st>>>(m, e0, slot, row);
 }
 
 }  // namespace hpsg

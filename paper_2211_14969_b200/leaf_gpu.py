@@ -61,7 +61,7 @@ EXPORTED = ["hps_gpu_create", "hps_gpu_destroy", "hps_gpu_last_error", "hps_gpu_
             "hps_gpu_set_fault_injection", "hps_host_alloc", "hps_host_free", "hps_gpu_version",
             "hps_gpu_sample_crystal", "hps_gpu_residual", "hps_gpu_residual_device",
             "hps_gpu_reduced_bsr_pattern", "hps_gpu_assemble_reduced_bsr",
-            "hps_gpu_assemble_reduced_bsr_device"]
+            "hps_gpu_assemble_reduced_bsr_device", "hps_gpu_scatter_indices"]
 
 
 def lib():
@@ -85,7 +85,7 @@ def lib():
                      "hps_gpu_get_info", "hps_gpu_get_timing", "hps_gpu_reset_timing",
                      "hps_gpu_sample_crystal", "hps_gpu_residual", "hps_gpu_residual_device",
                      "hps_gpu_reduced_bsr_pattern", "hps_gpu_assemble_reduced_bsr",
-                     "hps_gpu_assemble_reduced_bsr_device"):
+                     "hps_gpu_assemble_reduced_bsr_device", "hps_gpu_scatter_indices"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -229,6 +229,15 @@ class LeafStage:
         rp = np.empty(na + 1, np.int64); ci = np.empty(max(nnz.value, 1), np.int32)
         self._check(lib().hps_gpu_reduced_pattern(self._h, C.byref(nnz), _ptr(rp), _ptr(ci)))
         return rp, ci[:nnz.value]
+
+    def scatter_indices(self, e0=0, e1=None):
+        """Per-leaf scatter map (hps_gpu_scatter_indices): slot (n, nb, nb) int64 positions
+        in the CSR values (-1 = not in the reduced matrix) and row (n, nb) active rows."""
+        e1 = self.n_leaves if e1 is None else e1
+        n = max(e1 - e0, 0)
+        slot = np.empty((n, self.n_b, self.n_b), np.int64); row = np.empty((n, self.n_b), np.int64)
+        self._check(lib().hps_gpu_scatter_indices(self._h, e0, e1, _ptr(slot), _ptr(row)))
+        return slot, row
 
     def assemble_reduced(self, T, w, g_bnd):
         rp, ci = self.reduced_pattern()

@@ -48,6 +48,27 @@ struct DevBuf {
   template <class T> T* as() const { return static_cast<T*>(ptr); }
 };
 
+// Pinned host staging (the per-leaf status words): a D2H into caller memory that may be
+// pageable would block the host thread inside the chunk loop and serialise the pipeline.
+struct HostBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  ~HostBuf() { release(); }
+  void release() {
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+  cudaError_t ensure(size_t n) {
+    if (n <= bytes) return cudaSuccess;
+    release();
+    cudaError_t e = cudaHostAlloc(&ptr, n, cudaHostAllocPortable);
+    if (e == cudaSuccess) bytes = n;
+    return e;
+  }
+  template <class T> T* as() const { return static_cast<T*>(ptr); }
+};
+
 // ---- 1-D Chebyshev primitives -------
 // Same formulas and summation order as the CPU oracle (bit-identical tables).
 void cheb_tables(int p, double a, std::vector<double>& Ds, std::vector<double>& D2) {
@@ -192,6 +213,7 @@ struct hps_gpu_ctx {
   int n_leaves = 0;
   int chunk = 0;
   int k2_ctas = 2;               // co-resident K2 CTAs per SM (occupancy query at create)
+  int io_pieces = std::getenv("HPS_IO_PIECES") ? std::atoi(std::getenv("HPS_IO_PIECES")) : 4;
   size_t per_leaf = 0;
   std::string err;
   double k2 = 0.0;
@@ -231,6 +253,7 @@ struct hps_gpu_ctx {
   DevBuf field_off, field_cent;   // K0 crystal sampler: node offsets, centres
   DevBuf res_flux, res_pl, res_pe, res_in;   // K6 residual scratch
   int store_e0 = -1, store_e1 = -1;
+  HostBuf h_status;               // pinned staging of status[] (see HostBuf)
 
   ~hps_gpu_ctx() {
     for (auto e : tev) cudaEventDestroy(e);
@@ -659,6 +682,35 @@ static int check_range(hps_gpu_ctx* ctx, int e0, int e1) {
   return HPS_OK;
 }
 
+// Host-buffer transfer schedule (piece sizes, each <= chunk) so the H2D of piece i+1 and the
+// D2H of piece i-1 overlap the compute of piece i.  Streaming (range > workspace chunk):
+// full chunks, remainder last (measured best at C4: one-wave pieces lose more to per-launch
+// imbalance than they save in exposed copies).  Range fits: a one-wave first piece (its H2D
+// is exposed), a one-wave last piece (its D2H is exposed), the middle in >= io_pieces-2
+// pieces of whole waves of resident CTAs (C2: e2e 134k -> 151k leaves/s).  'store' keeps one
+// chunk (its factors stay resident).
+static std::vector<int> io_schedule(int total, int chunk, int wave, int io_pieces, bool store) {
+  std::vector<int> out;
+  if (total <= 0) return out;
+  wave = std::max(1, std::min(wave, chunk));
+  if (store || io_pieces <= 1 || total > chunk) {
+    for (int r = total; r > 0; r -= chunk) out.push_back(std::min(r, chunk));
+    return out;
+  }
+  const int first = std::min(wave, total);
+  const int last = std::min(wave, total - first);
+  int mid = total - first - last;
+  out.push_back(first);
+  if (mid > 0) {
+    const int nm = std::max((mid + chunk - 1) / chunk, std::max(1, io_pieces - 2));
+    int piece = (mid + nm - 1) / nm;
+    piece = std::min(chunk, (piece + wave - 1) / wave * wave);
+    for (; mid > 0; mid -= piece) out.push_back(std::min(mid, piece));
+  }
+  if (last > 0) out.push_back(last);
+  return out;
+}
+
 int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, const double* f,
                      double* T, double* w, double* S, int32_t* status) {
   if (!ctx) return HPS_ERR_PARAM;
@@ -680,19 +732,14 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
   }
   if (S) CK(ctx->uinv.ensure(size_t(4 * ctx->sms) * 4096 * 8));
   const size_t nis = size_t(d.ni) * d.nb;
-  // Transfer pipeline granularity: at least ~4 chunks (whole waves of resident CTAs) so the
-  // H2D of chunk i+1 and the D2H of chunk i-1 overlap the compute of chunk i even when the
-  // whole range fits the workspace.  'store' keeps one chunk (its factors stay resident).
-  int io_chunk = chunk;
-  if (ctx->desc.storage != HPS_STORAGE_STORE) {
-    const int slots = ctx->k2_ctas * ctx->sms;
-    const int quarter = (e1 - e0 + 3) / 4;
-    io_chunk = std::min(chunk, std::max(slots, (quarter + slots - 1) / slots * slots));
-  }
+  const std::vector<int> pieces =
+      io_schedule(e1 - e0, chunk, ctx->k2_ctas * ctx->sms, ctx->io_pieces,
+                  ctx->desc.storage == HPS_STORAGE_STORE);
+  CK(ctx->h_status.ensure(size_t(e1 - e0) * 4));
   reset_timing(ctx);
-  int ci = 0;
-  for (int c0 = e0; c0 < e1; c0 += io_chunk, ++ci) {
-    const int n = std::min(io_chunk, e1 - c0);
+  int c0 = e0;
+  for (int ci = 0; ci < int(pieces.size()); c0 += pieces[ci], ++ci) {
+    const int n = pieces[ci];
     const int k = ci & 1;
     const size_t off = size_t(c0 - e0);
     CK(cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_in_free[k], 0));
@@ -721,13 +768,15 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
     CK(cudaMemcpyAsync(T + off * nb2, ctx->out_T[k].ptr, n * nb2 * 8, cudaMemcpyDeviceToHost, ctx->s_d2h));
     CK(cudaMemcpyAsync(w + off * d.nb, ctx->out_w[k].ptr, n * size_t(d.nb) * 8, cudaMemcpyDeviceToHost,
                        ctx->s_d2h));
-    CK(cudaMemcpyAsync(status + off, ctx->out_st[k].ptr, n * 4, cudaMemcpyDeviceToHost, ctx->s_d2h));
+    CK(cudaMemcpyAsync(ctx->h_status.as<int32_t>() + off, ctx->out_st[k].ptr, n * 4, cudaMemcpyDeviceToHost,
+                       ctx->s_d2h));
     if (S)
       CK(cudaMemcpyAsync(S + off * nis, ctx->out_S[k].ptr, n * nis * 8, cudaMemcpyDeviceToHost, ctx->s_d2h));
     CK(cudaEventRecord(ctx->ev_out_free[k], ctx->s_d2h));
   }
   CK(cudaStreamSynchronize(ctx->s_d2h));
   CK(cudaStreamSynchronize(ctx->s_comp));
+  std::memcpy(status, ctx->h_status.ptr, size_t(e1 - e0) * 4);
   finish_timing(ctx);
   if (ctx->desc.storage == HPS_STORAGE_STORE) {
     ctx->store_e0 = e0;
@@ -858,6 +907,7 @@ int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b
     const int quarter = (e1 - e0 + 3) / 4;
     io_chunk = std::min(chunk, std::max(slots, (quarter + slots - 1) / slots * slots));
   }
+  CK(ctx->h_status.ensure(size_t(e1 - e0) * 4));
   reset_timing(ctx);
   int ci = 0;
   for (int c0 = e0; c0 < e1; c0 += io_chunk, ++ci) {
@@ -919,11 +969,13 @@ int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b
     CK(cudaEventRecord(ctx->ev_out_ready[k], st));
     CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_out_ready[k], 0));
     CK(cudaMemcpyAsync(u + off * pp, ctx->out_u[k].ptr, n * pp * 8, cudaMemcpyDeviceToHost, ctx->s_d2h));
-    CK(cudaMemcpyAsync(status + off, ctx->out_st[k].ptr, n * 4, cudaMemcpyDeviceToHost, ctx->s_d2h));
+    CK(cudaMemcpyAsync(ctx->h_status.as<int32_t>() + off, ctx->out_st[k].ptr, n * 4, cudaMemcpyDeviceToHost,
+                       ctx->s_d2h));
     CK(cudaEventRecord(ctx->ev_out_free[k], ctx->s_d2h));
   }
   CK(cudaStreamSynchronize(ctx->s_d2h));
   CK(cudaStreamSynchronize(ctx->s_comp));
+  std::memcpy(status, ctx->h_status.ptr, size_t(e1 - e0) * 4);
   finish_timing(ctx);
   std::vector<int> bad;
   for (int i = 0; i < e1 - e0; ++i)

@@ -706,6 +706,11 @@ static std::vector<int> io_schedule(int total, int chunk, int wave, int io_piece
     int piece = (mid + nm - 1) / nm;
     piece = std::min(chunk, (piece + wave - 1) / wave * wave);
     for (; mid > 0; mid -= piece) out.push_back(std::min(mid, piece));
+    // fold a fragment shorter than half a wave into the previous middle piece
+    if (out.size() > 2 && out.back() < wave / 2 && out[out.size() - 2] + out.back() <= chunk) {
+      out[out.size() - 2] += out.back();
+      out.pop_back();
+    }
   }
   if (last > 0) out.push_back(last);
   return out;

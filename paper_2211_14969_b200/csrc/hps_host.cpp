@@ -254,6 +254,7 @@ struct hps_gpu_ctx {
   DevBuf res_flux, res_pl, res_pe, res_in;   // K6 residual scratch
   int store_e0 = -1, store_e1 = -1;
   HostBuf h_status;               // pinned staging of status[] (see HostBuf)
+  HostBuf h_T[2], h_w[2];         // pinned staging of T/w pieces for pageable caller buffers
 
   ~hps_gpu_ctx() {
     for (auto e : tev) cudaEventDestroy(e);
@@ -716,6 +717,15 @@ static std::vector<int> io_schedule(int total, int chunk, int wave, int io_piece
   return out;
 }
 
+static bool host_pinned(const void* ptr) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
 int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, const double* f,
                      double* T, double* w, double* S, int32_t* status) {
   if (!ctx) return HPS_ERR_PARAM;
@@ -741,12 +751,32 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
       io_schedule(e1 - e0, chunk, ctx->k2_ctas * ctx->sms, ctx->io_pieces,
                   ctx->desc.storage == HPS_STORAGE_STORE);
   CK(ctx->h_status.ensure(size_t(e1 - e0) * 4));
+  // A D2H into pageable memory blocks the host thread until it completes, which would
+  // serialise the pieces: pageable T/w land in pinned double buffers instead and are copied
+  // out on the host while the next piece computes.
+  const bool stage = !pieces.empty() && !(host_pinned(T) && host_pinned(w));
+  if (stage) {
+    const int maxp = *std::max_element(pieces.begin(), pieces.end());
+    for (int i = 0; i < 2; ++i) {
+      CK(ctx->h_T[i].ensure(size_t(maxp) * nb2 * 8));
+      CK(ctx->h_w[i].ensure(size_t(maxp) * d.nb * 8));
+    }
+  }
+  auto drain = [&](int ci, size_t off, int n) -> cudaError_t {
+    cudaError_t e = cudaEventSynchronize(ctx->ev_out_free[ci & 1]);
+    if (e != cudaSuccess) return e;
+    std::memcpy(T + off * nb2, ctx->h_T[ci & 1].ptr, size_t(n) * nb2 * 8);
+    std::memcpy(w + off * d.nb, ctx->h_w[ci & 1].ptr, size_t(n) * d.nb * 8);
+    return cudaSuccess;
+  };
   reset_timing(ctx);
   int c0 = e0;
   for (int ci = 0; ci < int(pieces.size()); c0 += pieces[ci], ++ci) {
     const int n = pieces[ci];
     const int k = ci & 1;
     const size_t off = size_t(c0 - e0);
+    double* T_dst = stage ? ctx->h_T[k].as<double>() : T + off * nb2;
+    double* w_dst = stage ? ctx->h_w[k].as<double>() : w + off * d.nb;
     CK(cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_in_free[k], 0));
     CK(cudaMemcpyAsync(ctx->in_b[k].ptr, b + off * pp, n * pp * 8, cudaMemcpyHostToDevice, ctx->s_h2d));
     CK(cudaMemcpyAsync(ctx->in_f[k].ptr, f + off * pp, n * pp * 8, cudaMemcpyHostToDevice, ctx->s_h2d));
@@ -770,17 +800,21 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
     CK(cudaEventRecord(ctx->ev_in_free[k], ctx->s_comp));
     CK(cudaEventRecord(ctx->ev_out_ready[k], ctx->s_comp));
     CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_out_ready[k], 0));
-    CK(cudaMemcpyAsync(T + off * nb2, ctx->out_T[k].ptr, n * nb2 * 8, cudaMemcpyDeviceToHost, ctx->s_d2h));
-    CK(cudaMemcpyAsync(w + off * d.nb, ctx->out_w[k].ptr, n * size_t(d.nb) * 8, cudaMemcpyDeviceToHost,
-                       ctx->s_d2h));
+    CK(cudaMemcpyAsync(T_dst, ctx->out_T[k].ptr, n * nb2 * 8, cudaMemcpyDeviceToHost, ctx->s_d2h));
+    CK(cudaMemcpyAsync(w_dst, ctx->out_w[k].ptr, n * size_t(d.nb) * 8, cudaMemcpyDeviceToHost, ctx->s_d2h));
     CK(cudaMemcpyAsync(ctx->h_status.as<int32_t>() + off, ctx->out_st[k].ptr, n * 4, cudaMemcpyDeviceToHost,
                        ctx->s_d2h));
     if (S)
       CK(cudaMemcpyAsync(S + off * nis, ctx->out_S[k].ptr, n * nis * 8, cudaMemcpyDeviceToHost, ctx->s_d2h));
     CK(cudaEventRecord(ctx->ev_out_free[k], ctx->s_d2h));
+    if (stage && ci > 0) CK(drain(ci - 1, off - size_t(pieces[ci - 1]), pieces[ci - 1]));
   }
   CK(cudaStreamSynchronize(ctx->s_d2h));
   CK(cudaStreamSynchronize(ctx->s_comp));
+  if (stage) {
+    const int last = int(pieces.size()) - 1;
+    CK(drain(last, size_t(c0 - e0) - size_t(pieces[last]), pieces[last]));
+  }
   std::memcpy(status, ctx->h_status.ptr, size_t(e1 - e0) * 4);
   finish_timing(ctx);
   if (ctx->desc.storage == HPS_STORAGE_STORE) {

@@ -175,6 +175,9 @@ class LeafStage:
         b = _f64(b, (-1, pp)); f = _f64(f, (-1, pp))
         n = b.shape[0]
         if out is None:
+            # pageable: the library stages it through pinned double buffers (a fresh pinned
+            # allocation per call costs more than it saves; reuse PinnedArray for speed,
+            # tools/py_condense_timing.py)
             T = np.empty((n, self.n_b, self.n_b)); w = np.empty((n, self.n_b))
         else:
             T, w = out
@@ -264,6 +267,30 @@ class LeafStage:
         vals = np.empty((ci.size, q, q)); rhs = np.empty((rp.size - 1) * q)
         self._check(lib().hps_gpu_assemble_reduced_bsr(self._h, _ptr(T), _ptr(w), _ptr(g_bnd), _ptr(vals), _ptr(rhs)))
         return rp, ci, vals, rhs
+
+
+class _PinnedOwner:
+    def __init__(self, ptr):
+        self.ptr = ptr
+
+    def __del__(self):
+        try:
+            lib().hps_host_free(C.c_void_p(self.ptr))
+        except Exception:
+            pass
+
+
+def pinned_empty(shape, dtype=np.float64):
+    """numpy array in pinned host memory (hps_host_alloc), freed when the last view of it
+    is garbage-collected."""
+    count = int(np.prod(shape))
+    n = max(count * np.dtype(dtype).itemsize, 1)
+    ptr = lib().hps_host_alloc(n)
+    if not ptr:
+        raise CudaError("hps_host_alloc failed")
+    buf = (C.c_char * n).from_address(ptr)
+    buf._owner = _PinnedOwner(ptr)
+    return np.frombuffer(buf, dtype=dtype, count=count).reshape(shape)
 
 
 class PinnedArray:

@@ -13,7 +13,9 @@
  *       HPS_OK 0, HPS_ERR_RESONANCE 1 (see status[]), HPS_ERR_PARAM 2,
  *       HPS_ERR_CUDA 3.  hps_gpu_last_error(ctx) returns the message.
  *   - Ownership: the library owns device memory and streams; the caller owns
- *     every host buffer (pinned memory from hps_host_alloc gives overlap).
+ *     every host buffer (pinned memory from hps_host_alloc gives full overlap;
+ *     pageable T/w outputs of hps_gpu_condense are staged through library-owned
+ *     pinned double buffers, status[] always is).
  *   - Threading: one ctx per GPU, driven by one host thread; calls on distinct
  *     ctxs are concurrent-safe; one ctx is not reentrant (parallel.hpp's
  *     per-worker scratch rule).

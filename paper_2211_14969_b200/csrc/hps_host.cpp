@@ -255,6 +255,7 @@ struct hps_gpu_ctx {
   int store_e0 = -1, store_e1 = -1;
   HostBuf h_status;               // pinned staging of status[] (see HostBuf)
   HostBuf h_T[2], h_w[2];         // pinned staging of T/w pieces for pageable caller buffers
+  HostBuf h_u[2];                 // same for leaf_solve's u
 
   ~hps_gpu_ctx() {
     for (auto e : tev) cudaEventDestroy(e);
@@ -947,6 +948,14 @@ int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b
     io_chunk = std::min(chunk, std::max(slots, (quarter + slots - 1) / slots * slots));
   }
   CK(ctx->h_status.ensure(size_t(e1 - e0) * 4));
+  const bool stage = e1 > e0 && !host_pinned(u);   // see hps_gpu_condense
+  if (stage)
+    for (int i = 0; i < 2; ++i) CK(ctx->h_u[i].ensure(size_t(std::min(io_chunk, e1 - e0)) * pp * 8));
+  auto drain = [&](int ci, size_t off, int n) -> cudaError_t {
+    cudaError_t e = cudaEventSynchronize(ctx->ev_out_free[ci & 1]);
+    if (e == cudaSuccess) std::memcpy(u + off * pp, ctx->h_u[ci & 1].ptr, size_t(n) * pp * 8);
+    return e;
+  };
   reset_timing(ctx);
   int ci = 0;
   for (int c0 = e0; c0 < e1; c0 += io_chunk, ++ci) {
@@ -1007,13 +1016,20 @@ int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b
     CK(cudaEventRecord(ctx->ev_in_free[k], st));
     CK(cudaEventRecord(ctx->ev_out_ready[k], st));
     CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_out_ready[k], 0));
-    CK(cudaMemcpyAsync(u + off * pp, ctx->out_u[k].ptr, n * pp * 8, cudaMemcpyDeviceToHost, ctx->s_d2h));
+    CK(cudaMemcpyAsync(stage ? ctx->h_u[k].as<double>() : u + off * pp, ctx->out_u[k].ptr, n * pp * 8,
+                       cudaMemcpyDeviceToHost, ctx->s_d2h));
     CK(cudaMemcpyAsync(ctx->h_status.as<int32_t>() + off, ctx->out_st[k].ptr, n * 4, cudaMemcpyDeviceToHost,
                        ctx->s_d2h));
     CK(cudaEventRecord(ctx->ev_out_free[k], ctx->s_d2h));
+    if (stage && ci > 0) CK(drain(ci - 1, off - size_t(io_chunk), io_chunk));
   }
   CK(cudaStreamSynchronize(ctx->s_d2h));
   CK(cudaStreamSynchronize(ctx->s_comp));
+  if (stage) {
+    const int last = ci - 1;
+    const size_t loff = size_t(last) * io_chunk;
+    CK(drain(last, loff, (e1 - e0) - int(loff)));
+  }
   std::memcpy(status, ctx->h_status.ptr, size_t(e1 - e0) * 4);
   finish_timing(ctx);
   std::vector<int> bad;

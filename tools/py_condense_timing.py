@@ -27,3 +27,13 @@ with G.LeafStage(p, nx, nx, 100.0) as st:
             ts.append(time.perf_counter() - t)
         dt = min(ts[1:])
         print(f"{name:<28} {dt*1e3:7.2f} ms  {n/dt:9.0f} leaves/s")
+
+    v = np.random.default_rng(0).uniform(-1, 1, (n, nb))
+    for name in ("leaf_solve pageable u",):
+        ts = []
+        for i in range(4):
+            t = time.perf_counter()
+            st.leaf_solve(b, f, v)
+            ts.append(time.perf_counter() - t)
+        dt = min(ts[1:])
+        print(f"{name:<28} {dt*1e3:7.2f} ms  {n/dt:9.0f} leaves/s")

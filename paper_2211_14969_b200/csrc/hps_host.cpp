@@ -256,6 +256,7 @@ struct hps_gpu_ctx {
   HostBuf h_status;               // pinned staging of status[] (see HostBuf)
   HostBuf h_T[2], h_w[2];         // pinned staging of T/w pieces for pageable caller buffers
   HostBuf h_u[2];                 // same for leaf_solve's u
+  bool no_stage = std::getenv("HPS_NO_STAGE") != nullptr;   // A/B knob
 
   ~hps_gpu_ctx() {
     for (auto e : tev) cudaEventDestroy(e);
@@ -755,7 +756,7 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
   // A D2H into pageable memory blocks the host thread until it completes, which would
   // serialise the pieces: pageable T/w land in pinned double buffers instead and are copied
   // out on the host while the next piece computes.
-  const bool stage = !pieces.empty() && !(host_pinned(T) && host_pinned(w));
+  const bool stage = !pieces.empty() && !ctx->no_stage && !(host_pinned(T) && host_pinned(w));
   if (stage) {
     const int maxp = *std::max_element(pieces.begin(), pieces.end());
     for (int i = 0; i < 2; ++i) {
@@ -948,7 +949,7 @@ int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b
     io_chunk = std::min(chunk, std::max(slots, (quarter + slots - 1) / slots * slots));
   }
   CK(ctx->h_status.ensure(size_t(e1 - e0) * 4));
-  const bool stage = e1 > e0 && !host_pinned(u);   // see hps_gpu_condense
+  const bool stage = e1 > e0 && !ctx->no_stage && !host_pinned(u);   // see hps_gpu_condense
   if (stage)
     for (int i = 0; i < 2; ++i) CK(ctx->h_u[i].ensure(size_t(std::min(io_chunk, e1 - e0)) * pp * 8));
   auto drain = [&](int ci, size_t off, int n) -> cudaError_t {

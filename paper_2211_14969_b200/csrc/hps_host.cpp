@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <thread>
 #include <memory>
 #include <set>
 #include <string>
@@ -719,6 +720,28 @@ static std::vector<int> io_schedule(int total, int chunk, int wave, int io_piece
   return out;
 }
 
+// Host copy-out of a staged piece: split across threads above 8 MB (one thread's memcpy into
+// freshly faulted pageable pages runs far below the host's memory bandwidth).
+static void par_memcpy(void* dst, const void* src, size_t bytes) {
+  const size_t kMin = size_t(8) << 20;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int nt = int(std::min<size_t>(std::min(8u, hw), std::max<size_t>(1, bytes / kMin)));
+  if (nt <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  const size_t part = (bytes + nt - 1) / nt;
+  std::vector<std::thread> th;
+  for (int i = 1; i < nt; ++i) {
+    const size_t o = size_t(i) * part;
+    if (o >= bytes) break;
+    th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
+                                      std::min(part, bytes - o)); });
+  }
+  std::memcpy(dst, src, std::min(part, bytes));
+  for (auto& t : th) t.join();
+}
+
 static bool host_pinned(const void* ptr) {
   cudaPointerAttributes at{};
   if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
@@ -767,7 +790,7 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
   auto drain = [&](int ci, size_t off, int n) -> cudaError_t {
     cudaError_t e = cudaEventSynchronize(ctx->ev_out_free[ci & 1]);
     if (e != cudaSuccess) return e;
-    std::memcpy(T + off * nb2, ctx->h_T[ci & 1].ptr, size_t(n) * nb2 * 8);
+    par_memcpy(T + off * nb2, ctx->h_T[ci & 1].ptr, size_t(n) * nb2 * 8);
     std::memcpy(w + off * d.nb, ctx->h_w[ci & 1].ptr, size_t(n) * d.nb * 8);
     return cudaSuccess;
   };
@@ -954,7 +977,7 @@ int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b
     for (int i = 0; i < 2; ++i) CK(ctx->h_u[i].ensure(size_t(std::min(io_chunk, e1 - e0)) * pp * 8));
   auto drain = [&](int ci, size_t off, int n) -> cudaError_t {
     cudaError_t e = cudaEventSynchronize(ctx->ev_out_free[ci & 1]);
-    if (e == cudaSuccess) std::memcpy(u + off * pp, ctx->h_u[ci & 1].ptr, size_t(n) * pp * 8);
+    if (e == cudaSuccess) par_memcpy(u + off * pp, ctx->h_u[ci & 1].ptr, size_t(n) * pp * 8);
     return e;
   };
   reset_timing(ctx);

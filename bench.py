@@ -188,9 +188,9 @@ def run_reference(args, cfg):
 
 def k2_kernel_name(p):
     """The condensation kernel the C-ABI dispatches for p (hps_kernels.h small_condense_preferred)."""
-    if 4 <= p <= 12 and os.environ.get("HPS_SMALL", "") != "0":
+    if 4 <= p <= 12:
         return "k2s_condense_kernel (register-resident, fused assembly, DFMA f64)"
-    if (p - 2) ** 2 + 4 * (p - 1) <= 640 and os.environ.get("HPS_LOCKSTEP", "") != "0":
+    if (p - 2) ** 2 + 4 * (p - 1) <= 640:
         return "g128::k2_lu_lockstep_kernel (4 leaves per CTA, DMMA f64)"
     return "g256::k2_lu_schur_kernel (DMMA f64)"
 

@@ -100,10 +100,6 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global" HPS_L2_PREFETCH " [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
 // ---- mbarrier helpers (shared::cta) ----
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
@@ -128,42 +124,6 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
       : "memory");
 }
 
-__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, unsigned bytes) {
-  asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n" ::"r"(
-                   smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-// Bulk (TMA-engine) copy global -> shared, completion counted on an mbarrier in bytes.
-__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gmem_src, unsigned bytes,
-                                         unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(smem_dst)),
-      "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-}
-
-// Long waits (cross-group hand-offs): try_wait with a suspend-time hint so idle warps
-// do not spin on the issue slots the working group needs.
-__device__ __forceinline__ void mbar_wait_sleep(unsigned long long* bar, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "WAITS_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-      " @!p bra WAITS_%=;\n}\n" ::"r"(smem_u32(bar)),
-      "r"(parity), "r"(1000000u)
-      : "memory");
-}
-
-__device__ __forceinline__ long long globaltimer() {
-  long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
-
 // 1/x for a pivot: MUFU.RCP64H seed + two Newton steps, no special-case branch (IEEE
 // division and __drcp_rn carry one, and a CALL to a slow path, on the pivot chain).
 // Relative error ~1 ulp; x is a nonzero finite pivot (a zero or tiny pivot is a
@@ -175,11 +135,6 @@ __device__ __forceinline__ double fast_rcp(double x) {
   r = __fma_rn(r, e, r);
   e = __fma_rn(-x, r, 1.0);
   return __fma_rn(r, e, r);
-}
-
-// Order-preserving bits of a non-negative double (for integer atomicMax).
-__device__ __forceinline__ unsigned long long dbits(double x) {
-  return static_cast<unsigned long long>(__double_as_longlong(x));
 }
 
 }  // namespace hpsg

@@ -214,7 +214,7 @@ struct hps_gpu_ctx {
   int n_leaves = 0;
   int chunk = 0;
   int k2_ctas = 2;               // co-resident K2 CTAs per SM (occupancy query at create)
-  int io_pieces = std::getenv("HPS_IO_PIECES") ? std::atoi(std::getenv("HPS_IO_PIECES")) : 4;
+  int io_pieces = 4;             // host-buffer transfer pieces when the range fits (io_schedule)
   size_t per_leaf = 0;
   std::string err;
   double k2 = 0.0;
@@ -225,31 +225,28 @@ struct hps_gpu_ctx {
   DevBuf m_elem_edges, m_edge_elems, m_edge_sides, m_edge_cols, m_edge_ne, m_edge_off;
   cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_in_ready[2]{}, ev_in_free[2]{}, ev_out_ready[2]{}, ev_out_free[2]{};
+  // Last use of the shared device scratch (ws, linv, perm, norms, minratio) by any call,
+  // on whichever stream it ran: device-resident calls run on the caller's stream, host-buffer
+  // calls on s_comp, so every entry waits on it and every exit records it.
+  cudaEvent_t ev_scratch = nullptr;
   std::vector<cudaEvent_t> tev;  // timing events, 3 per chunk (before K1, K1|K2, after K2)
-  int tslots = 0;                // chunk triplets recorded since the last reset
+  int tslots = 0;                // chunk triplets recorded since the last fold
+  hps_gpu_timing_t tacc{};       // intervals folded out of the event ring since the last reset
   int tkernels = 0;              // kernels launched since the last reset
   float ms_scatter = 0.0f;
   hps_gpu_timing_t timing{};
   bool has_inject = false;
-  bool phase_timers = std::getenv("HPS_PHASE_TIMERS") != nullptr;
-  // K1 materialises the operator (default); HPS_FUSED=1 evaluates the tile C-inits in K2
-  // instead (first-touch assembly, no workspace writes by K1; slower in r01 measurements).
-  bool fused = std::getenv("HPS_FUSED") != nullptr;
-  // Panel/GEMM lookahead kernel for condense (HPS_LOOKAHEAD=1); the default 2-leaves-per-SM
-  // kernel measured faster on C2/C3/C4 in round 1.
-  bool lookahead = std::getenv("HPS_LOOKAHEAD") && std::getenv("HPS_LOOKAHEAD")[0] == '1';
   // Lock-step multi-leaf K2 kernel (4 leaves per CTA, panels aligned): measured faster for
-  // the 4-warp build (C2: 14.05 -> 13.25 ms), slower for the 8-warp build (C3/C4), so by
-  // default only where the 4-warp build runs.  HPS_LOCKSTEP=0/1 disables/forces it.
-  int lockstep_env = std::getenv("HPS_LOCKSTEP") ? std::atoi(std::getenv("HPS_LOCKSTEP")) : -1;
-  long long dephase_ns = std::getenv("HPS_DEPHASE_NS") ? std::atoll(std::getenv("HPS_DEPHASE_NS")) : 0;
-  // HPS_K2_CFG=128|256 forces the K2 build (default: by leaf size, hps_kernels.h use_g128).
-  int max_ctas = std::getenv("HPS_K2_CTAS") ? std::atoi(std::getenv("HPS_K2_CTAS")) : 0;
-  int force_cfg = std::getenv("HPS_K2_CFG") ? std::atoi(std::getenv("HPS_K2_CFG")) : 0;
-  // K2s (register-resident, assembly fused) where it measured faster (p <= 12, not 10);
-  // HPS_SMALL=0 disables it, HPS_SMALL=1 forces it for every supported p.  The blocked
-  // K1+K2 path still runs where the factors must stay resident (S_solve, 'store').
-  int small_env = std::getenv("HPS_SMALL") ? std::atoi(std::getenv("HPS_SMALL")) : -1;
+  // the 4-warp build (C2: 14.05 -> 13.25 ms), slower for the 8-warp build (C3/C4), so it runs
+  // wherever the 4-warp build does.
+  // Experiment knobs (phase timers, forced K2 build/path, K2s trace, no staging) exist only in
+  // HPS_DEBUG_KNOBS builds (`make EXTRA=-DHPS_DEBUG_KNOBS`), read once at ctx creation.
+  bool phase_timers = false;
+  int lockstep_env = -1;
+  int force_cfg = 0;
+  int small_env = -1;
+  bool k2s_trace = false;
+  bool no_stage = false;
   DevBuf phase_buf;
   DevBuf field_off, field_cent;   // K0 crystal sampler: node offsets, centres
   DevBuf res_flux, res_pl, res_pe, res_in;   // K6 residual scratch
@@ -257,7 +254,6 @@ struct hps_gpu_ctx {
   HostBuf h_status;               // pinned staging of status[] (see HostBuf)
   HostBuf h_T[2], h_w[2];         // pinned staging of T/w pieces for pageable caller buffers
   HostBuf h_u[2];                 // same for leaf_solve's u
-  bool no_stage = std::getenv("HPS_NO_STAGE") != nullptr;   // A/B knob
 
   ~hps_gpu_ctx() {
     for (auto e : tev) cudaEventDestroy(e);
@@ -267,6 +263,7 @@ struct hps_gpu_ctx {
       if (ev_out_ready[i]) cudaEventDestroy(ev_out_ready[i]);
       if (ev_out_free[i]) cudaEventDestroy(ev_out_free[i]);
     }
+    if (ev_scratch) cudaEventDestroy(ev_scratch);
     if (s_comp) cudaStreamDestroy(s_comp);
     if (s_h2d) cudaStreamDestroy(s_h2d);
     if (s_d2h) cudaStreamDestroy(s_d2h);
@@ -332,35 +329,53 @@ int resonance_error(hps_gpu_ctx* ctx, const std::vector<int>& bad) {
 
 void reset_timing(hps_gpu_ctx* ctx) {
   ctx->tslots = 0;
+  ctx->tacc = hps_gpu_timing_t{};
   ctx->tkernels = 0;
   ctx->ms_scatter = 0.0f;
 }
 
+// Move the intervals of the recorded event triplets into ctx->tacc and empty the ring
+// (synchronizes on the last recorded event).
+void fold_timing(hps_gpu_ctx* ctx) {
+  const int n = ctx->tslots;
+  if (n == 0) return;
+  hps_gpu_timing_t& t = ctx->tacc;
+  cudaEventSynchronize(ctx->tev[3 * n - 1]);
+  for (int c = 0; c < n; ++c) {
+    float a = 0, b = 0;
+    cudaEventElapsedTime(&a, ctx->tev[3 * c], ctx->tev[3 * c + 1]);
+    cudaEventElapsedTime(&b, ctx->tev[3 * c + 1], ctx->tev[3 * c + 2]);
+    t.ms_assemble += a;
+    t.ms_lu_schur += b;
+  }
+  float span = 0;
+  cudaEventElapsedTime(&span, ctx->tev[0], ctx->tev[3 * n - 1]);
+  t.ms_total += span;
+  t.chunks += n;
+  ctx->tslots = 0;
+}
+
+// Timing-event slot for the next chunk.  The ring is bounded (kTimingSlots triplets): a
+// long loop of device-resident calls that never resets folds it instead of growing it.
+constexpr int kTimingSlots = 256;
+int next_timing_slot(hps_gpu_ctx* ctx) {
+  if (ctx->tslots >= kTimingSlots) fold_timing(ctx);
+  return ctx->tslots++;
+}
+
 // Sum the per-chunk CUDA-event intervals recorded since the last reset.
 void finish_timing(hps_gpu_ctx* ctx) {
-  hps_gpu_timing_t t{};
-  const int n = ctx->tslots;
-  t.chunks = n;
+  fold_timing(ctx);
+  hps_gpu_timing_t t = ctx->tacc;
   t.kernels = ctx->tkernels;
   t.ms_scatter = ctx->ms_scatter;
-  if (n > 0) {
-    cudaEventSynchronize(ctx->tev[3 * n - 1]);
-    for (int c = 0; c < n; ++c) {
-      float a = 0, b = 0;
-      cudaEventElapsedTime(&a, ctx->tev[3 * c], ctx->tev[3 * c + 1]);
-      cudaEventElapsedTime(&b, ctx->tev[3 * c + 1], ctx->tev[3 * c + 2]);
-      t.ms_assemble += a;
-      t.ms_lu_schur += b;
-    }
-    cudaEventElapsedTime(&t.ms_total, ctx->tev[0], ctx->tev[3 * n - 1]);
-  }
   t.ms_total += t.ms_scatter;
   ctx->timing = t;
 }
 
 // Device pipeline for one chunk of `n` leaves starting at element e (K1 + K2).
 bool use_small(const hps_gpu_ctx* ctx, bool need_factors) {
-  if (ctx->small_env == 0 || need_factors || ctx->fused || ctx->lookahead || ctx->phase_timers) return false;
+  if (ctx->small_env == 0 || need_factors || ctx->phase_timers) return false;
   return ctx->small_env == 1 ? hpsg::small_condense_supported(ctx->d.p)
                              : hpsg::small_condense_preferred(ctx->d.p);
 }
@@ -370,7 +385,7 @@ void enqueue_condense_chunk(hps_gpu_ctx* ctx, int e, int n, const double* d_b, c
                             bool need_factors) {
   const LeafDims& d = ctx->d;
   const int* inj = ctx->has_inject ? ctx->inject_all.as<int>() + e : nullptr;
-  const int ci = ctx->tslots++;
+  const int ci = next_timing_slot(ctx);
   if (use_small(ctx, need_factors)) {
     // K2s: one kernel, assembly + norm + elimination + T/w/status (no workspace).
     ctx->tkernels += 1;
@@ -388,7 +403,7 @@ void enqueue_condense_chunk(hps_gpu_ctx* ctx, int e, int n, const double* d_b, c
     a.minratio = ctx->minratio.as<double>();
     a.norms = ctx->norms.as<double>();
     a.inject = inj;
-    const bool trace = std::getenv("HPS_K2S_TRACE") != nullptr;
+    const bool trace = ctx->k2s_trace;
     const int NW = hpsg::small_condense_warps(d.p), BW = hpsg::small_condense_block(d.p);
     const int NPB = (d.ni + BW - 1) / BW;
     const size_t ntr = size_t(3) * NPB * NW + NPB + 2 * NW + 1;
@@ -427,16 +442,11 @@ void enqueue_condense_chunk(hps_gpu_ctx* ctx, int e, int n, const double* d_b, c
     }
     return;
   }
-  ctx->tkernels += ctx->fused ? 2 : 3;
+  ctx->tkernels += 3;
   cudaEventRecord(ctx->timing_event(3 * ci), st);
-  if (ctx->fused) {
-    // K1 fused into K2 (first-touch assembly): only ||A_ii|| runs as its own kernel.
-    hpsg::launch_aii_norm(d, ctx->D2.as<double>(), ctx->k2, d_b, inj, ctx->norms.as<double>(), n, st);
-  } else {
-    hpsg::launch_assemble(d, ctx->rowcode.as<int>(), ctx->colcode.as<int>(), ctx->Ds.as<double>(),
-                          ctx->D2.as<double>(), ctx->k2, d_b, d_f, ctx->ws.as<double>(),
-                          ctx->norms.as<double>(), inj, n, st);
-  }
+  hpsg::launch_assemble(d, ctx->rowcode.as<int>(), ctx->colcode.as<int>(), ctx->Ds.as<double>(),
+                        ctx->D2.as<double>(), ctx->k2, d_b, d_f, ctx->ws.as<double>(),
+                        ctx->norms.as<double>(), inj, n, st);
   cudaEventRecord(ctx->timing_event(3 * ci + 1), st);
   hpsg::LuArgs a;
   a.d = d;
@@ -449,18 +459,7 @@ void enqueue_condense_chunk(hps_gpu_ctx* ctx, int e, int n, const double* d_b, c
   a.status = d_status;
   a.minratio = ctx->minratio.as<double>();
   a.factor = 1;
-  a.dephase_ns = ctx->dephase_ns;
-  a.max_ctas_per_sm = ctx->max_ctas;
-  a.fused = ctx->fused ? 1 : 0;
-  a.lookahead = (ctx->lookahead && !ctx->fused) ? 1 : 0;
   a.lockstep = ctx->lockstep_env == 1 || (ctx->lockstep_env != 0 && hpsg::use_g128(d, ctx->force_cfg));
-  a.rowcode = ctx->rowcode.as<int>();
-  a.colcode = ctx->colcode.as<int>();
-  a.Ds = ctx->Ds.as<double>();
-  a.D2 = ctx->D2.as<double>();
-  a.k2 = ctx->k2;
-  a.b = d_b;
-  a.f = d_f;
   a.inject = inj;
   if (ctx->phase_timers) {
     ctx->phase_buf.ensure(size_t(ctx->chunk) * 16 * sizeof(long long));
@@ -476,12 +475,6 @@ void enqueue_condense_chunk(hps_gpu_ctx* ctx, int e, int n, const double* d_b, c
     double sum[16] = {0};
     for (int i = 0; i < n; ++i)
       for (int k = 0; k < 16; ++k) sum[k] += double(h[size_t(i) * 16 + k]);
-    if (a.lookahead)
-      std::fprintf(stderr,
-                   "[hps LA cycles/leaf] GEMM: wait-done %.3g window %.3g post-panel %.3g D-rows %.3g | "
-                   "panel: wait-ready %.3g work %.3g\n",
-                   sum[0] / n, sum[1] / n, sum[2] / n, sum[5] / n, sum[3] / n, sum[4] / n);
-    else
     std::fprintf(stderr,
                  "[hps phase cycles/leaf] U-part %.3g  L-part %.3g  panel %.3g (strips %.3g [start %.3g "
                  "columns %.3g end %.3g] upd-U %.3g upd-L %.3g)  linv %.3g  trailing %.3g\n",
@@ -543,6 +536,16 @@ int hps_gpu_create(int device, const hps_leaf_desc* desc, hps_gpu_ctx** out) {
   if (D.storage != HPS_STORAGE_RECOMPUTE && D.storage != HPS_STORAGE_STORE)
     return reject(HPS_ERR_PARAM, "ParameterError: unknown storage policy");
   hps_gpu_ctx* c = ctx.get();
+#ifdef HPS_DEBUG_KNOBS
+  auto env_int = [](const char* k, int dflt) { const char* v = std::getenv(k); return v ? std::atoi(v) : dflt; };
+  c->io_pieces = env_int("HPS_IO_PIECES", c->io_pieces);
+  c->phase_timers = std::getenv("HPS_PHASE_TIMERS") != nullptr;
+  c->lockstep_env = env_int("HPS_LOCKSTEP", -1);
+  c->force_cfg = env_int("HPS_K2_CFG", 0);
+  c->small_env = env_int("HPS_SMALL", -1);
+  c->k2s_trace = std::getenv("HPS_K2S_TRACE") != nullptr;
+  c->no_stage = std::getenv("HPS_NO_STAGE") != nullptr;
+#endif
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return reject(HPS_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
@@ -580,6 +583,7 @@ int hps_gpu_create(int device, const hps_leaf_desc* desc, hps_gpu_ctx** out) {
     CK(cudaStreamCreateWithFlags(&c->s_comp, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->ev_scratch, cudaEventDisableTiming));
     for (int i = 0; i < 2; ++i) {
       CK(cudaEventCreateWithFlags(&c->ev_in_ready[i], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_in_free[i], cudaEventDisableTiming));
@@ -732,13 +736,20 @@ static void par_memcpy(void* dst, const void* src, size_t bytes) {
   }
   const size_t part = (bytes + nt - 1) / nt;
   std::vector<std::thread> th;
-  for (int i = 1; i < nt; ++i) {
-    const size_t o = size_t(i) * part;
-    if (o >= bytes) break;
-    th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
-                                      std::min(part, bytes - o)); });
+  size_t done = std::min(part, bytes);   // bytes from here on are copied by the calling thread
+  try {
+    for (int i = 1; i < nt; ++i) {
+      const size_t o = size_t(i) * part;
+      if (o >= bytes) break;
+      th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
+                                        std::min(part, bytes - o)); });
+      done = std::min(bytes, o + part);
+    }
+  } catch (...) {   // no thread could be started: nothing may propagate out of the C-ABI
   }
   std::memcpy(dst, src, std::min(part, bytes));
+  if (done < bytes) std::memcpy(static_cast<char*>(dst) + done, static_cast<const char*>(src) + done,
+                                bytes - done);
   for (auto& t : th) t.join();
 }
 
@@ -795,6 +806,7 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
     return cudaSuccess;
   };
   reset_timing(ctx);
+  CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_scratch, 0));
   int c0 = e0;
   for (int ci = 0; ci < int(pieces.size()); c0 += pieces[ci], ++ci) {
     const int n = pieces[ci];
@@ -834,6 +846,7 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
     CK(cudaEventRecord(ctx->ev_out_free[k], ctx->s_d2h));
     if (stage && ci > 0) CK(drain(ci - 1, off - size_t(pieces[ci - 1]), pieces[ci - 1]));
   }
+  CK(cudaEventRecord(ctx->ev_scratch, ctx->s_comp));
   CK(cudaStreamSynchronize(ctx->s_d2h));
   CK(cudaStreamSynchronize(ctx->s_comp));
   if (stage) {
@@ -859,16 +872,26 @@ int hps_gpu_condense_device(hps_gpu_ctx* ctx, int32_t e0, int32_t n, const doubl
   if (!ctx) return HPS_ERR_PARAM;
   if (int rc = check_range(ctx, e0, e0 + n)) return rc;
   CK(cudaSetDevice(ctx->device));
+  if (n > 0 && (!d_b || !d_f || !d_T || !d_w || !d_status))
+    return ctx->fail(HPS_ERR_PARAM, "ParameterError: null device buffer");
+  const bool store = ctx->desc.storage == HPS_STORAGE_STORE;
+  if (store && n > ctx->chunk)
+    return ctx->fail(HPS_ERR_PARAM, "ParameterError: store policy range exceeds resident factors");
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->s_comp;
   const LeafDims& d = ctx->d;
   const size_t pp = size_t(d.p) * d.p, nb2 = size_t(d.nb) * d.nb;
-  int ci = 0;
-  for (int c0 = 0; c0 < n; c0 += ctx->chunk, ++ci) {
+  CK(cudaStreamWaitEvent(st, ctx->ev_scratch, 0));
+  for (int c0 = 0; c0 < n; c0 += ctx->chunk) {
     const int m = std::min(ctx->chunk, n - c0);
     enqueue_condense_chunk(ctx, e0 + c0, m, d_b + c0 * pp, d_f + c0 * pp, d_T + c0 * nb2,
-                           d_w + size_t(c0) * d.nb, d_status + c0, st,
-                           ctx->desc.storage == HPS_STORAGE_STORE);
+                           d_w + size_t(c0) * d.nb, d_status + c0, st, store);
     CK(cudaGetLastError());
+  }
+  CK(cudaEventRecord(ctx->ev_scratch, st));
+  // 'store': the kept factors are now those of [e0, e0 + n) (one chunk, checked above).
+  if (store) {
+    ctx->store_e0 = e0;
+    ctx->store_e1 = e0 + n;
   }
   return HPS_OK;
 }
@@ -981,6 +1004,7 @@ int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b
     return e;
   };
   reset_timing(ctx);
+  CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_scratch, 0));
   int ci = 0;
   for (int c0 = e0; c0 < e1; c0 += io_chunk, ++ci) {
     const int n = std::min(io_chunk, e1 - c0);
@@ -994,7 +1018,7 @@ int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b
     CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_in_ready[k], 0));
     CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_out_free[k], 0));
     cudaStream_t st = ctx->s_comp;
-    const int slot = ctx->tslots++;
+    const int slot = next_timing_slot(ctx);
     ctx->tkernels += store ? 3 : 4;
     cudaEventRecord(ctx->timing_event(3 * slot), st);
     hpsg::LuArgs a;
@@ -1047,6 +1071,7 @@ int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b
     CK(cudaEventRecord(ctx->ev_out_free[k], ctx->s_d2h));
     if (stage && ci > 0) CK(drain(ci - 1, off - size_t(io_chunk), io_chunk));
   }
+  CK(cudaEventRecord(ctx->ev_scratch, ctx->s_comp));
   CK(cudaStreamSynchronize(ctx->s_d2h));
   CK(cudaStreamSynchronize(ctx->s_comp));
   if (stage) {

@@ -18,10 +18,6 @@ void launch_assemble(const LeafDims& d, const int* rowcode, const int* colcode, 
                      const double* D2, double k2, const double* b, const double* f, double* ws,
                      double* norms, const int* inject, int n_leaves, cudaStream_t st);
 
-// ||A_ii||_inf only (fused-assembly condense path).
-void launch_aii_norm(const LeafDims& d, const double* D2, double k2, const double* b,
-                     const int* inject, double* norms, int n_leaves, cudaStream_t st);
-
 // K1 (leaf-solve variant): [A_ii | f_i - A_ib v] with no D rows (rows ni..Rpad zero).
 void launch_assemble_solve(const LeafDims& d, const int* rowcode, const int* colcode,
                            const double* Ds, const double* D2, double k2, const double* b,
@@ -46,20 +42,7 @@ struct LuArgs {
   double* minratio;     // per leaf, nullable
   int factor;           // 1: factor A_ii then trailing columns; 0: trailing columns only
   long long* phase_cycles = nullptr;  // optional 8 counters per leaf (profiling)
-  long long dephase_ns = 0;           // start delay of the second CTA on each SM
-  int lookahead = 0;                  // condense: panel/GEMM warp-specialised kernel
   int lockstep = 0;                   // factor: lock-step multi-leaf kernel (panels aligned)
-  int max_ctas_per_sm = 0;            // >0: cap the persistent grid below the occupancy
-  // Fused first-touch assembly (fused = 1): tile C-inits are evaluated from the
-  // operator definition instead of loaded from a K1-materialised workspace.
-  int fused = 0;
-  const int* rowcode = nullptr;
-  const int* colcode = nullptr;
-  const double* Ds = nullptr;
-  const double* D2 = nullptr;
-  double k2 = 0.0;
-  const double* b = nullptr;           // p*p per leaf
-  const double* f = nullptr;           // p*p per leaf
   const int* inject = nullptr;         // per leaf, nullable
 };
 // Two builds of k2_lu_schur.cu: g256 (8-warp CTAs, R <= 2048) and g128 (4-warp CTAs,
@@ -84,7 +67,7 @@ inline bool use_g128(const LeafDims& d, int force) {
   return d.R <= 640;
 }
 inline void launch_lu_schur(const LuArgs& a, int n_leaves, cudaStream_t st, int force = 0) {
-  if (use_g128(a.d, force) && !a.lookahead) g128::launch_lu_schur(a, n_leaves, st);
+  if (use_g128(a.d, force)) g128::launch_lu_schur(a, n_leaves, st);
   else g256::launch_lu_schur(a, n_leaves, st);
 }
 // Co-resident K2 CTAs per SM for leaves of shape d (occupancy query, not an assumption).

@@ -234,12 +234,6 @@ void launch_assemble(const LeafDims& d, const int* rowcode, const int* colcode, 
   k1_aii_norm_kernel<<<n_leaves, 256, 0, st>>>(d, D2, k2, b, inject, norms);
 }
 
-void launch_aii_norm(const LeafDims& d, const double* D2, double k2, const double* b,
-                     const int* inject, double* norms, int n_leaves, cudaStream_t st) {
-  if (n_leaves <= 0) return;
-  k1_aii_norm_kernel<<<n_leaves, 256, 0, st>>>(d, D2, k2, b, inject, norms);
-}
-
 void launch_assemble_solve(const LeafDims& d, const int* rowcode, const int* colcode,
                            const double* Ds, const double* D2, double k2, const double* b,
                            const double* f, const double* v, double* ws, double* norms,

@@ -88,11 +88,9 @@ constexpr int MAX_NSLOT = 8;
 static_assert(MAX_NSLOT * NT >= HPS_MAX_ROWS, "strip rows per thread");         // strip rows per thread: R <= 2048 (p <= 45)
 constexpr int MAX_RPAD = HPS_MAX_ROWS + 128;  // perm entries (tile gathers may run past R)
 
-// A group of 256 threads (8 warps) sharing a named barrier.  The one-leaf-per-CTA kernel
-// uses the whole CTA (barrier 0); the lookahead kernel runs a GEMM group (threads 0-255,
-// barrier 1) and a panel group (threads 256-511, barrier 2) side by side.
-// Thread index within its group of NT threads (the tile/panel helpers are group-local:
-// one-leaf kernel, lookahead kernel groups, lock-step multi-leaf kernel groups).
+// A group of NT threads sharing a named barrier.  The one-leaf-per-CTA kernel uses the whole
+// CTA (barrier 0); the lock-step multi-leaf kernel runs several groups (barriers 1..).
+// gtid(): thread index within its group (the tile/panel helpers are group-local).
 __device__ __forceinline__ int gtid() { return static_cast<int>(threadIdx.x) & (NT - 1); }
 
 struct Grp {
@@ -129,11 +127,6 @@ using TileU = Tile<64, 64>;
 #endif
 constexpr int TLM = TileL::WM * 32;  // L-part / D-row tile rows
 constexpr int TUN = TileU::WN * 32;  // U-part tile columns
-#if HPS_NT == 256
-// Lookahead kernel (1 CTA/SM, more shared memory): 4 stages.
-using TileL2 = Tile<128, 64, 16, 4>;
-using TileU2 = Tile<64, 128, 16, 4>;
-#endif
 constexpr int LS_U = TUN + 4;        // Linv-apply staging of a 64 x TUN U tile (== 4 mod 16)
 constexpr int cmax(int a, int b) { return a > b ? a : b; }
 // The pipeline region doubles as panel scratch: in-panel update blocks (2 x 32 x 36),
@@ -299,42 +292,6 @@ __device__ __forceinline__ void acc_load(Acc& acc, const CRow& crow, int nrows) 
         acc.v[mi][ni][1] = 0.0;
       }
     }
-  }
-}
-
-// Original operator entries of a tile (fused first-touch assembly): logical rows
-// base+r gathered through perm, columns c0 + tile column.
-struct Orig {
-  const int* rowcode;
-  const int* colcode;
-  const double* Ds;
-  const double* D2;
-  double k2;
-  const double* bl;
-  const double* fl;
-  int p;
-  bool inj;
-};
-
-template <class TL>
-__device__ __forceinline__ void acc_init_orig(Acc& acc, const Orig& o, const LeafDims& d,
-                                              const short* perm, int base, int c0, int nrows) {
-  int cc[8];
-#pragma unroll
-  for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) cc[2 * ni + h] = col_code_of(c0 + acc_col<TL>(ni) + h, d.p, d.ni, d.tb0, d.nb);
-#pragma unroll
-  for (int mi = 0; mi < 4; ++mi) {
-    const int r = acc_row<TL>(mi);
-    const int phys = perm[base + r];
-    const int rc = r < nrows ? row_code_of(phys, d.p, d.ni, d.R) : (3 << 16);
-    const bool zrow = o.inj && phys == 0;
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni)
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-        acc.v[mi][ni][h] = aug_value(rc, cc[2 * ni + h], o.p, o.Ds, o.D2, o.k2, o.bl, o.fl, zrow);
   }
 }
 
@@ -825,16 +782,6 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf, const Gr
   G.sync();
   double minpiv = INFINITY;  // meaningful on thread 0
   long long* pc = a.phase_cycles ? a.phase_cycles + (size_t)leaf * 16 : nullptr;
-  Orig orig;
-  orig.rowcode = a.rowcode;
-  orig.colcode = a.colcode;
-  orig.Ds = a.Ds;
-  orig.D2 = a.D2;
-  orig.k2 = a.k2;
-  orig.bl = a.b ? a.b + (size_t)leaf * d.p * d.p : nullptr;
-  orig.fl = a.f ? a.f + (size_t)leaf * d.p * d.p : nullptr;
-  orig.p = d.p;
-  orig.inj = a.inject && a.inject[leaf];
   long long t_phase = clock64();
 
   const double* M = L.M;
@@ -858,10 +805,7 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf, const Gr
         const int nr = min(TLM, d.R - rt);
         auto crow = [=](int i) -> double* { return L.M + (size_t)perm[rt + i] * ld + c0; };
         Acc acc;
-        auto init = [&](Acc& x) {
-          if (a.fused) acc_init_orig<TileL>(x, orig, d, perm, rt, c0, nr);
-          else acc_load<TileL>(x, crow, nr);
-        };
+        auto init = [&](Acc& x) { acc_load<TileL>(x, crow, nr); };
         auto arow = lrow(rt);
         auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + c0; };
         // columns c0 + w .. c0 + 63 of the last block are A_ii padding (zero): no DMMA there
@@ -884,10 +828,7 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf, const Gr
     for (int ct = ct_begin; ct < ct_end; ct += TUN) {
       auto crow = [=](int i) -> double* { return L.M + (size_t)perm[c0 + i] * ld + ct; };
       Acc acc;
-      auto init = [&](Acc& x) {
-        if (a.fused) acc_init_orig<TileU>(x, orig, d, perm, c0, ct, 64);
-        else acc_load<TileU>(x, crow, 64);
-      };
+      auto init = [&](Acc& x) { acc_load<TileU>(x, crow, 64); };
       auto arow = lrow(c0);
       auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + ct; };
       // Real (non-padding) columns of this tile: A_ii columns end at ni, the trailing block
@@ -914,10 +855,7 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf, const Gr
       const int nr = min(TLM, d.R - rt);
       auto crow = [=](int i) -> double* { return L.M + (size_t)perm[rt + i] * ld + c0; };
       Acc acc;
-      auto init = [&](Acc& x) {
-        if (a.fused) acc_init_orig<TileL>(x, orig, d, perm, rt, c0, nr);
-        else acc_load<TileL>(x, crow, nr);
-      };
+      auto init = [&](Acc& x) { acc_load<TileL>(x, crow, nr); };
       auto arow = lrow(rt);
       auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + c0; };
       tile_mma<TileL>(G, acc, init, arow, brow, d.ni, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk,
@@ -957,9 +895,6 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf, const Gr
 }
 
 // Persistent: grid = 2 CTAs per SM, each walks leaves blockIdx.x, +gridDim.x, ...
-// The second CTA of every SM (blockIdx >= gridDim/2; classic placement puts b and
-// b + #SM on one SM) starts `dephase_ns` late so the two co-resident leaves are not in
-// their (latency-bound) panel phases at the same time.
 constexpr int CTAS_PER_SM = HPS_CTAS;
 
 template <int NSLOT>
@@ -974,10 +909,6 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k2_lu_schur_kernel(LuArgs a, 
     sm->gchunk = 0;
   }
   __syncthreads();
-  if (a.dephase_ns > 0 && blockIdx.x >= (gridDim.x + 1) / 2) {
-    const long long t0 = globaltimer();
-    while (globaltimer() - t0 < a.dephase_ns) __nanosleep(20000);
-  }
   for (int leaf = blockIdx.x; leaf < n_leaves; leaf += gridDim.x) process_leaf<NSLOT>(a, sm, leaf);
 }
 
@@ -1014,237 +945,6 @@ __global__ void __launch_bounds__(NT * NGRP, 1) k2_lu_lockstep_kernel(LuArgs a, 
   }
 }
 
-#if HPS_NT == 256
-// ===========================================================================
-// Lookahead kernel: one CTA (16 warps) per SM and leaf.  Warps 0-7 (GEMM group) run all
-// tile jobs; warps 8-15 (panel group) factor panel J while the GEMM group works on what
-// does not depend on it:
-//   window of panel J : U(J-1, c >= J+1)                      (block row J-1, Linv epilogue)
-//                       partial L(J+1), K in [0, c0_J), on the rows not pivoted before
-//                       panel J (perm snapshot) -- this also pre-computes A - L U for
-//                       the rows that become panel J's pivot rows
-//   after panel J     : U(J, J+1) = Linv_J * partial           (no GEMM, Linv only)
-//                       L(J+1) remainder, K = block J (64)      -> panel J+1 may start
-// Hand-offs are two mbarriers (GEMM -> panel "column ready", panel -> GEMM "panel done").
-// Each output element is computed by the same tile code as in k2_lu_schur_kernel; only the
-// split of K between the partial and the remainder pass differs for the L part.
-// ===========================================================================
-constexpr int NT_LA = 2 * NT;
-constexpr int PAN_DBL = 2 * 32 * 36 + 4 * 2048;   // update Ls/X + strip hand-off (>= 64*65 for Linv)
-constexpr int PIPE_LA = cmax(cmax(TileL2::NS * TileL2::STAGE, TileU2::NS * TileU2::STAGE), 64 * LS_U);
-
-struct SmemLA {
-  double pipe[PIPE_LA];
-  double pan[PAN_DBL];
-  alignas(16) double wrow[2][NT / 32][8];
-  unsigned long long redk[2][NT / 32];
-  unsigned long long full[MAX_NSTAGE];
-  unsigned long long empty[MAX_NSTAGE];
-  unsigned long long ready_bar;   // GEMM -> panel: column J fully updated
-  unsigned long long done_bar;    // panel -> GEMM: panel J + Linv_J done
-  unsigned gchunk;
-  short perm[MAX_RPAD];
-  short iperm[MAX_RPAD];
-  short snap[MAX_RPAD];           // perm snapshot: candidate rows of the running panel
-};
-
-__device__ __forceinline__ void group_release(const Grp& G, unsigned long long* bar) {
-  __threadfence_block();
-  G.sync();
-  if (G.tid == 0) mbar_arrive(bar);
-}
-
-template <int NSLOT>
-__device__ void process_leaf_la(const LuArgs& a, SmemLA* sm, const int leaf, const unsigned pbase) {
-  const LeafDims d = a.d;
-  const bool gemm = threadIdx.x < NT;
-  const Grp G{gemm ? (int)threadIdx.x : (int)threadIdx.x - NT, gemm ? 1 : 2};
-  double* Mw = a.ws + (size_t)leaf * d.leaf_stride;
-  double* Linv = a.linv + (size_t)leaf * d.nblk * 4096;
-  const int ld = d.ld;
-  for (int i = threadIdx.x; i < MAX_RPAD; i += NT_LA) {
-    const short v = i < d.Rpad ? (short)i : (short)(d.Rpad - 1);
-    sm->perm[i] = v;
-    sm->snap[i] = v;
-    sm->iperm[i] = (short)i;
-  }
-  __syncthreads();
-  // optional timers (thread 0 of each group): GEMM 0 wait-done 1 window 2 post-panel 5 D rows;
-  // panel 3 wait-ready 4 factor+linv
-  long long* pcl = a.phase_cycles ? a.phase_cycles + (size_t)leaf * 16 : nullptr;
-  long long* pc = nullptr;      // (in-panel sub-phase marks off)
-  long long t_phase = 0;
-  long long tl = clock64();
-  auto mark = [&](int slot) {
-    if (pcl && G.tid == 0) {
-      const long long now = clock64();
-      pcl[slot] += now - tl;
-      tl = now;
-    }
-  };
-
-  if (!gemm) {
-    // ------------------------------ panel group ------------------------------
-    LeafCtx L;
-    L.M = Mw;
-    L.ld = ld;
-    L.R = d.R;
-    L.ni = d.ni;
-    L.perm = sm->perm;
-    L.iperm = sm->iperm;
-    L.scratch = sm->pan;
-    L.wrow = &sm->wrow[0][0][0];
-    L.redk = &sm->redk[0][0];
-    double minpiv = INFINITY;
-    for (int J = 0; J < d.nblk; ++J) {
-      const int c0 = 64 * J, w = min(64, d.ni - c0);
-      mark(4);
-      mbar_wait_sleep(&sm->ready_bar, (pbase + J) & 1u);
-      mark(3);
-      panel_factor<NSLOT>(G, L, c0, w, minpiv, pc, t_phase);
-      panel_linv(G, L, c0, w, Linv + (size_t)J * 4096);
-      group_release(G, &sm->done_bar);
-    }
-    if (G.tid == 0) {
-      const double nrm = a.norms[leaf];
-      const double ratio = nrm > 0.0 ? minpiv / nrm : 0.0;
-      if (a.minratio) a.minratio[leaf] = ratio;
-      a.status[leaf] = (ratio >= 1e-12) ? 0 : 1;
-    }
-  } else {
-    // ------------------------------ GEMM group -------------------------------
-    const double* M = Mw;
-    const short* perm = sm->perm;
-    const short* snap = sm->snap;
-    const int ct_end = d.tb0 + 64 * d.ntb;
-    auto utile = [&](int J, int ct, int K, int ncols) {   // U(J, ct..): full GEMM + Linv_J
-      const int c0 = 64 * J, w = min(64, d.ni - c0);
-      auto crow = [=](int i) -> double* { return Mw + (size_t)perm[c0 + i] * ld + ct; };
-      auto arow = [=](int i) -> const double* { return M + (size_t)perm[c0 + i] * ld; };
-      auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + ct; };
-      Acc acc;
-      auto init = [&](Acc& x) { acc_load<TileU2>(x, crow, 64); };
-      tile_mma<TileU2>(G, acc, init, arow, brow, K, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
-      linv_apply<TRI_LOWER>(G, acc, Linv + (size_t)J * 4096, sm->pipe);
-      acc_store<TileU2>(acc, crow, w, ncols);
-    };
-    // column 0 holds original values: panel 0 may start at once
-    group_release(G, &sm->ready_bar);
-    for (int J = 0; J < d.nblk; ++J) {
-      const int c0 = 64 * J;
-      // ---- window of panel J ----
-      if (J >= 1)
-        for (int ct = c0 + 64; ct < ct_end; ct += 128) utile(J - 1, ct, c0 - 64, min(128, ct_end - ct));
-      if (J + 1 < d.nblk && c0 > 0) {   // partial L(J+1): rows of the snapshot, K = c0
-        const int c1 = c0 + 64;
-        for (int rt = c0; rt < d.R; rt += 128) {
-          const int nr = min(128, d.R - rt);
-          auto crow = [=](int i) -> double* { return Mw + (size_t)snap[rt + i] * ld + c1; };
-          auto arow = [=](int i) -> const double* { return M + (size_t)snap[rt + i] * ld; };
-          auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + c1; };
-          Acc acc;
-          auto init = [&](Acc& x) { acc_load<TileL2>(x, crow, nr); };
-          tile_mma<TileL2>(G, acc, init, arow, brow, c0, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
-          acc_store<TileL2>(acc, crow, nr, 64);
-        }
-      }
-      mark(1);
-      mbar_wait_sleep(&sm->done_bar, (pbase + J) & 1u);
-      mark(0);
-      // ---- after panel J ----
-      if (J + 1 < d.nblk) {
-        const int c1 = c0 + 64;
-        {   // U(J, J+1) = Linv_J * (partial values of the pivot rows)
-          auto crow = [=](int i) -> double* { return Mw + (size_t)perm[c0 + i] * ld + c1; };
-          Acc acc;
-          acc_load<TileU2>(acc, crow, 64);
-          linv_apply<TRI_LOWER>(G, acc, Linv + (size_t)J * 4096, sm->pipe);
-          acc_store<TileU2>(acc, crow, 64, 64);
-        }
-        __threadfence_block();
-        G.sync();
-        // L(J+1) remainder: rows [c1, R), K = block J
-        for (int rt = c1; rt < d.R; rt += 128) {
-          const int nr = min(128, d.R - rt);
-          auto crow = [=](int i) -> double* { return Mw + (size_t)perm[rt + i] * ld + c1; };
-          auto arow = [=](int i) -> const double* { return M + (size_t)perm[rt + i] * ld + c0; };
-          auto brow = [=](int k) -> const double* { return M + (size_t)perm[c0 + k] * ld + c1; };
-          Acc acc;
-          auto init = [&](Acc& x) { acc_load<TileL2>(x, crow, nr); };
-          tile_mma<TileL2>(G, acc, init, arow, brow, 64, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
-          acc_store<TileL2>(acc, crow, nr, 64);
-        }
-        // snapshot the candidate rows of panel J+1 for the next partial pass
-        for (int i = c1 + G.tid; i < d.Rpad; i += NT) sm->snap[i] = sm->perm[i];
-        group_release(G, &sm->ready_bar);
-      } else {
-        // last panel: U(J, trailing) with the full K = c0
-        for (int ct = d.tb0; ct < ct_end; ct += 128) utile(J, ct, c0, min(128, ct_end - ct));
-        __threadfence_block();
-        G.sync();
-      }
-      mark(2);
-    }
-    // D rows of the trailing columns: T = D_b - L21 U12 ; -w = -L21 (L^{-1} f)  (K = ni)
-    double* Tl = a.T_out + (size_t)leaf * d.nb * d.nb;
-    double* wl = a.w_out + (size_t)leaf * d.nb;
-    for (int tb = 0; tb < d.ntb; ++tb) {
-      const int c0 = d.tb0 + 64 * tb;
-      for (int rt = d.ni; rt < d.R; rt += 128) {
-        const int nr = min(128, d.R - rt);
-        auto crow = [=](int i) -> double* { return Mw + (size_t)perm[rt + i] * ld + c0; };
-        auto arow = [=](int i) -> const double* { return M + (size_t)perm[rt + i] * ld; };
-        auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + c0; };
-        Acc acc;
-        auto init = [&](Acc& x) { acc_load<TileL2>(x, crow, nr); };
-        tile_mma<TileL2>(G, acc, init, arow, brow, d.ni, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi) {
-          const int r = acc_row<TileL2>(mi);
-          if (r >= nr) continue;
-          const int trow = rt + r - d.ni;
-#pragma unroll
-          for (int ni2 = 0; ni2 < 4; ++ni2) {
-#pragma unroll
-            for (int hh = 0; hh < 2; ++hh) {
-              const int tc = 64 * tb + acc_col<TileL2>(ni2) + hh;
-              if (tc < d.nb) Tl[(size_t)trow * d.nb + tc] = acc.v[mi][ni2][hh];
-              else if (tc == d.nb) wl[trow] = -acc.v[mi][ni2][hh];
-            }
-          }
-        }
-      }
-    }
-    mark(5);
-  }
-  __syncthreads();
-  short* perm_g = a.perm + (size_t)leaf * d.Rpad;
-  for (int i = threadIdx.x; i < d.Rpad; i += NT_LA) perm_g[i] = sm->perm[i];
-  __syncthreads();
-}
-
-template <int NSLOT>
-__global__ void __launch_bounds__(NT_LA, 1) k2_lu_lookahead_kernel(LuArgs a, int n_leaves) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  SmemLA* sm = reinterpret_cast<SmemLA*>(smem_raw);
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < MAX_NSTAGE; ++s) {
-      mbar_init(&sm->full[s], NT);
-      mbar_init(&sm->empty[s], NT / 32);
-    }
-    mbar_init(&sm->ready_bar, 1);
-    mbar_init(&sm->done_bar, 1);
-    sm->gchunk = 0;
-  }
-  __syncthreads();
-  unsigned pbase = 0;   // panels completed by this CTA (mbarrier phase base)
-  for (int leaf = blockIdx.x; leaf < n_leaves; leaf += gridDim.x) {
-    process_leaf_la<NSLOT>(a, sm, leaf, pbase);
-    pbase += a.d.nblk;
-  }
-}
-
-#endif  // HPS_NT == 256
 
 size_t lu_smem_bytes() { return sizeof(Smem); }
 
@@ -1350,15 +1050,6 @@ static void launch_ns(const LuArgs& a, int n_leaves, cudaStream_t st) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-#if HPS_NT == 256
-  if (a.lookahead && a.factor && a.d.nb > 0) {
-    cudaFuncSetAttribute(k2_lu_lookahead_kernel<NSLOT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(SmemLA));
-    const int grid = n_leaves < sms ? n_leaves : sms;
-    k2_lu_lookahead_kernel<NSLOT><<<grid, NT_LA, sizeof(SmemLA), st>>>(a, n_leaves);
-    return;
-  }
-#endif
   if (a.lockstep && a.factor) {
     const int smem = int(SMEM_GRP * NGRP);
     cudaFuncSetAttribute(k2_lu_lockstep_kernel<NSLOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -1373,7 +1064,6 @@ static void launch_ns(const LuArgs& a, int n_leaves, cudaStream_t st) {
   // whole CTAs, each owning several leaves, waiting for a second wave).
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_lu_schur_kernel<NSLOT>, NT, sizeof(Smem));
-  if (a.max_ctas_per_sm > 0 && a.max_ctas_per_sm < per_sm) per_sm = a.max_ctas_per_sm;
   if (per_sm < 1) per_sm = 1;
   const int grid = n_leaves < per_sm * sms ? n_leaves : per_sm * sms;
   k2_lu_schur_kernel<NSLOT><<<grid, NT, sizeof(Smem), st>>>(a, n_leaves);

@@ -98,7 +98,28 @@ def _ptr(a):
 def _f64(a, shape=None):
     a = np.ascontiguousarray(a, dtype=np.float64)
     if shape is not None:
-        a = a.reshape(shape)
+        try:
+            a = a.reshape(shape)
+        except ValueError as e:
+            raise ParameterError(f"input of shape {a.shape} cannot be viewed as {shape}") from e
+    return a
+
+
+def _rows(a, n, name):
+    """Inputs handed to the C-ABI must cover exactly the n leaves of the call."""
+    if a.shape[0] != n:
+        raise ParameterError(f"{name}: {a.shape[0]} leaves given, {n} expected")
+    return a
+
+
+def _out(a, shape, dtype, name):
+    """Caller-provided outputs are written through raw pointers: they must be C-contiguous,
+    of the exact dtype and shape, and writeable (ParameterError otherwise)."""
+    if not isinstance(a, np.ndarray) or a.dtype != np.dtype(dtype) or tuple(a.shape) != tuple(shape) \
+            or not a.flags.c_contiguous or not a.flags.writeable:
+        got = (getattr(a, "shape", None), getattr(a, "dtype", None))
+        raise ParameterError(f"{name}: need a writeable C-contiguous {np.dtype(dtype)} array of shape "
+                             f"{tuple(shape)}, got {got}")
     return a
 
 
@@ -174,6 +195,9 @@ class LeafStage:
         pp = self.p * self.p
         b = _f64(b, (-1, pp)); f = _f64(f, (-1, pp))
         n = b.shape[0]
+        _rows(f, n, "f")
+        if e0 < 0 or e0 + n > self.n_leaves:
+            raise ParameterError(f"element range [{e0}, {e0 + n}) outside the mesh of {self.n_leaves} leaves")
         if out is None:
             # pageable: the library stages it through pinned double buffers (a fresh pinned
             # allocation per call costs more than it saves; reuse PinnedArray for speed,
@@ -181,6 +205,8 @@ class LeafStage:
             T = np.empty((n, self.n_b, self.n_b)); w = np.empty((n, self.n_b))
         else:
             T, w = out
+            _out(T, (n, self.n_b, self.n_b), np.float64, "out T")
+            _out(w, (n, self.n_b), np.float64, "out w")
         S = np.empty((n, self.n_i, self.n_b)) if want_S else None
         st = np.zeros(n, np.int32)
         rc = lib().hps_gpu_condense(self._h, e0, e0 + n, _ptr(b), _ptr(f), _ptr(T), _ptr(w), _ptr(S), _ptr(st))
@@ -210,6 +236,8 @@ class LeafStage:
         u_leaf (n_leaves x p^2): dict(r_int2, r_flux2, f_int2) (Eq. 7)."""
         pp = self.p * self.p
         b = _f64(b, (-1, pp)); f = _f64(f, (-1, pp)); u = _f64(u_leaf, (-1, pp))
+        for a, nm in ((b, "b"), (f, "f"), (u, "u")):
+            _rows(a, self.n_leaves, nm)
         out = np.zeros(3)
         self._check(lib().hps_gpu_residual(self._h, _ptr(b), _ptr(f), _ptr(u), _ptr(out)))
         return dict(r_int2=out[0], r_flux2=out[1], f_int2=out[2])
@@ -219,6 +247,9 @@ class LeafStage:
         pp = self.p * self.p
         b = _f64(b, (-1, pp)); f = _f64(f, (-1, pp)); v = _f64(v, (-1, self.n_b))
         n = b.shape[0]
+        _rows(f, n, "f"); _rows(v, n, "v")
+        if e0 < 0 or e0 + n > self.n_leaves:
+            raise ParameterError(f"element range [{e0}, {e0 + n}) outside the mesh of {self.n_leaves} leaves")
         u = np.empty((n, pp)); st = np.zeros(n, np.int32)
         rc = lib().hps_gpu_leaf_solve(self._h, e0, e0 + n, _ptr(b), _ptr(f), _ptr(v), _ptr(u), _ptr(st))
         self._check(rc, st, e0)
@@ -242,9 +273,17 @@ class LeafStage:
         self._check(lib().hps_gpu_scatter_indices(self._h, e0, e1, _ptr(slot), _ptr(row)))
         return slot, row
 
+    def _reduced_inputs(self, T, w, g_bnd):
+        T = _f64(T, (-1, self.n_b, self.n_b)); w = _f64(w, (-1, self.n_b)); g_bnd = _f64(g_bnd, (-1,))
+        _rows(T, self.n_leaves, "T"); _rows(w, self.n_leaves, "w")
+        ng = 2 * (self.nx * (self.p - 1) + 1) + 2 * (self.ny * (self.p - 1) + 1)
+        if g_bnd.size != ng:
+            raise ParameterError(f"g_bnd: {g_bnd.size} values given, {ng} expected ([S | N | W | E])")
+        return T, w, g_bnd
+
     def assemble_reduced(self, T, w, g_bnd):
         rp, ci = self.reduced_pattern()
-        T = _f64(T); w = _f64(w); g_bnd = _f64(g_bnd)
+        T, w, g_bnd = self._reduced_inputs(T, w, g_bnd)
         vals = np.empty(ci.size); rhs = np.empty(rp.size - 1)
         self._check(lib().hps_gpu_assemble_reduced(self._h, _ptr(T), _ptr(w), _ptr(g_bnd), _ptr(vals), _ptr(rhs)))
         return rp, ci, vals, rhs
@@ -263,7 +302,7 @@ class LeafStage:
         """assemble_reduced in BSR: (brow_ptr, bcol_idx, blocks[nnzb, q, q], rhs); the entries
         are bit-identical to assemble_reduced's CSR values."""
         q, rp, ci = self.reduced_bsr_pattern()
-        T = _f64(T); w = _f64(w); g_bnd = _f64(g_bnd)
+        T, w, g_bnd = self._reduced_inputs(T, w, g_bnd)
         vals = np.empty((ci.size, q, q)); rhs = np.empty((rp.size - 1) * q)
         self._check(lib().hps_gpu_assemble_reduced_bsr(self._h, _ptr(T), _ptr(w), _ptr(g_bnd), _ptr(vals), _ptr(rhs)))
         return rp, ci, vals, rhs

@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--leaf-solve", action=argparse.BooleanOptionalAction, default=True,
+                    help="also time batched leaf_solve (K5, recompute policy) on the workload")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
 
@@ -123,29 +125,78 @@ def gpu_index(local_rank):
     return str(local_rank)
 
 
-def cpu_baseline(cfg, seconds, threads=0):
-    """The CPU oracle (C++ restatement of SPEC batched_condense, OpenBLAS, all host
-    threads via the reference's parallel_for contract) on a bounded sample of the
-    same workload.  Returns (leaves/s, cores, sample description)."""
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def b_star(cfg):
+    """Resonant coefficient value of the workload: kappa^2 b* = lowest interior Dirichlet
+    eigenvalue of a leaf of side a, ~2 pi^2 / a^2 (189,575 at C4 vs 2 pi^2 98^2 = 189,571)."""
+    return 2.0 * np.pi ** 2 / (cfg["a"] ** 2 * max(cfg["kappa"], 1e-300) ** 2)
+
+
+def sample_order(cfg, b):
+    """Leaves for the CPU sample, most demanding first: those whose b range spans the resonant
+    b*, then the rest of the crystal (b not identically 1), then the b = 1 leaves; each group
+    in a fixed pseudo-random order."""
+    rng = np.random.default_rng(7)
+    bmin, bmax = b.min(axis=1), b.max(axis=1)
+    bs = b_star(cfg)
+    near = (bmin <= bs) & (bmax >= bs)
+    var = (bmin < 1.0) & ~near
+    rest = ~(near | var)
+    groups = [rng.permutation(np.nonzero(m)[0]) for m in (near, var, rest)]
+    return np.concatenate(groups), int(near.sum()), int((bmin < 1.0).sum())
+
+
+def cpu_baseline(cfg, seconds, b_all, T_dev=None, threads=0):
+    """The CPU oracle (C++ restatement of SPEC batched_condense, OpenBLAS, all host threads via
+    the reference's parallel_for contract) on a bounded sample of the same workload: the
+    sample starts with the near-resonant and crystal leaves (sample_order).  When the device
+    arm's T (all leaves of this rank, f = 0 so w = 0) is given, the sample doubles as a parity
+    check of the GPU output against the oracle (relative Frobenius per leaf, bar 1e-10).
+    Returns (leaves/s, cores, sample description, parity dict or None)."""
     from oracle import pyoracle as O
     cores = threads or O.hardware_workers()
     p = cfg["p"]
-    n_all = cfg["n_leaves"]
+    order, n_near, n_var = sample_order(cfg, b_all)
     batch = max(cores, 1)
-    done = 0
-    t_total = 0.0
-    e = 0
-    while t_total < seconds or done < 2 * batch:
-        e1 = min(n_all, e + batch)
-        b, f = leaf_inputs(cfg, e, e1)
+    done, t_total = 0, 0.0
+    errs, status_mismatch, minratio = [], 0, np.inf
+    f0 = np.zeros((batch, p * p))
+    while done < order.size and (t_total < seconds or done < 2 * batch):
+        ids = order[done:done + batch]
+        bb = np.ascontiguousarray(b_all[ids])
         t0 = time.perf_counter()
-        O.batched_condense(p, cfg["a"], cfg["kappa"], b, f, workers=cores, raise_on_resonance=False)
+        r = O.batched_condense(p, cfg["a"], cfg["kappa"], bb, f0[:ids.size], workers=cores,
+                               raise_on_resonance=False)
         t_total += time.perf_counter() - t0
-        done += e1 - e
-        e = e1 % n_all
-        if done >= n_all:
-            break
-    return done / t_total, cores, f"{done} of {n_all} leaves of {cfg['name']} (p={p}), {t_total:.1f} s wall"
+        done += ids.size
+        minratio = min(minratio, float(r["min_pivot_ratio"].min()))
+        if T_dev is not None:
+            Tg = T_dev[ids].reshape(ids.size, -1)
+            Tr = r["T"].reshape(ids.size, -1)
+            ok = r["status"] == 0
+            num = np.linalg.norm(Tg - Tr, axis=1)
+            den = np.maximum(np.linalg.norm(Tr, axis=1), 1e-300)
+            errs.extend((num / den)[ok].tolist())
+    sample = (f"{done} of {cfg['n_leaves']} leaves of {cfg['name']} (p={p}): the {min(done, n_near)} leaves "
+              f"whose b spans b*={b_star(cfg):.4g}, then crystal leaves ({n_var} with b != 1 in the mesh), "
+              f"{t_total:.1f} s wall")
+    parity = None
+    if T_dev is not None and errs:
+        parity = {"leaves": len(errs), "near_resonant_in_sample": int(min(done, n_near)),
+                  "max_relfro_T": max(errs), "median_relfro_T": float(np.median(errs)),
+                  "min_pivot_ratio": minratio, "bar": 1e-10, "pass": max(errs) <= 1e-10,
+                  "inputs": "device arm's T (crystal b, f=0) vs oracle on the CPU sample"}
+    return done / t_total, cores, sample, parity
 
 
 def run_reference(args, cfg):
@@ -155,14 +206,20 @@ def run_reference(args, cfg):
     from oracle import pyoracle as O
     cores = O.hardware_workers()
     p = cfg["p"]
-    # bounded sample per step: ~4 s of all-core work
-    b, f = leaf_inputs(cfg, 0, cores)
+    # bounded sample per step (~4 s of all-core work) from the same leaf order as the
+    # cpu_baseline leg: near-resonant leaves, then the crystal, then b = 1 leaves
+    b_all, _ = leaf_inputs(cfg, 0, cfg["n_leaves"])
+    order, _, _ = sample_order(cfg, b_all)
+    f = np.zeros((cores, p * p))
     t0 = time.perf_counter()
-    O.batched_condense(p, cfg["a"], cfg["kappa"], b, f, workers=cores, raise_on_resonance=False)
+    O.batched_condense(p, cfg["a"], cfg["kappa"], b_all[order[:cores]], f, workers=cores,
+                       raise_on_resonance=False)
     per_round = time.perf_counter() - t0
     rounds = max(1, int(4.0 / max(per_round, 1e-3)))
     n = min(cfg["n_leaves"], rounds * cores)
-    b, f = leaf_inputs(cfg, 0, n)
+    b = np.ascontiguousarray(b_all[order[:n]])
+    f = np.zeros_like(b)
+    del b_all
     for _ in range(args.warmup):
         O.batched_condense(p, cfg["a"], cfg["kappa"], b, f, workers=cores, raise_on_resonance=False)
     t0 = time.perf_counter()
@@ -170,7 +227,8 @@ def run_reference(args, cfg):
         O.batched_condense(p, cfg["a"], cfg["kappa"], b, f, workers=cores, raise_on_resonance=False)
     dt = (time.perf_counter() - t0) / args.steps
     v = n / dt
-    sample = f"{n} of {cfg['n_leaves']} leaves of {cfg['name']} per step"
+    sample = (f"{n} of {cfg['n_leaves']} leaves of {cfg['name']} per step (near-resonant and crystal "
+              f"leaves first); host CPU: {cpu_model()}")
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "leaves/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
@@ -178,7 +236,8 @@ def run_reference(args, cfg):
         "config": workload_config(cfg, args.gpus),
         "dof_per_s": v * cfg["N"] / cfg["n_leaves"],
         "tflops": v * P.flops_condense(p) / 1e12,
-        "cpu_baseline": {"value": v, "unit": "leaves/s", "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "leaves/s", "cores": cores, "kind": "port", "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": v, "unit": "leaves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "note": "reference has no implementation (SPEC + headers only); the arm times the C++ restatement "
                 "of SPEC batched_condense (oracle/, OpenBLAS, parallel_for over all host threads)",
@@ -300,7 +359,7 @@ def main():
         pT = G.PinnedArray((n, nb, nb)); pw = G.PinnedArray((n, nb))
         for _ in range(max(1, min(args.warmup, 2))):
             stage.condense(pb.array, pf.array, e0=e0, out=(pT.array, pw.array), raise_on_resonance=False)
-        k_e2e = max(1, min(args.steps, 3))
+        k_e2e = args.steps
         barrier()
         t0 = time.perf_counter()
         for _ in range(k_e2e):
@@ -314,6 +373,43 @@ def main():
                "steps": k_e2e, "api": "hps_gpu_condense (pinned host b,f -> T,w)"}
         for a in (pb, pf, pT, pw):
             a.free()
+
+    # ---- K5: batched leaf_solve (recompute policy) through the C-ABI ----
+    leaf_solve = None
+    if args.leaf_solve:
+        rng = np.random.default_rng(3)
+        v = rng.uniform(-1.0, 1.0, (n, nb))
+        pb = G.PinnedArray(b.shape); pb.array[:] = b
+        pf = G.PinnedArray(f.shape); pf.array[:] = f
+        pv = G.PinnedArray(v.shape); pv.array[:] = v
+        pu = G.PinnedArray((n, p * p))
+        stage.leaf_solve(pb.array, pf.array, pv.array, e0=e0, out=pu.array)   # warm-up
+        k_ls = max(1, min(args.steps, 3))
+        dev_ms, k1_ms, k2k5_ms = 0.0, 0.0, 0.0
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(k_ls):
+            stage.leaf_solve(pb.array, pf.array, pv.array, e0=e0, out=pu.array)
+            tl = stage.timing()
+            dev_ms += tl["ms_total"]; k1_ms += tl["ms_assemble"]; k2k5_ms += tl["ms_lu_schur"]
+        dt = max_over_ranks(time.perf_counter() - t0)
+        ni = (p - 2) ** 2
+        f_ls = P.flops_leaf_solve(p)
+        leaf_solve = {"api": "hps_gpu_leaf_solve (recompute: K1s assemble [A_ii | f - A_ib v], K2 LU + forward "
+                             "solve, K5 back substitution; pinned host b, f, v -> u)",
+                      "steps": k_ls, "e2e_leaves_per_s": cfg["n_leaves"] * k_ls / dt,
+                      "device_leaves_per_s": n * k_ls / (dev_ms / 1e3),
+                      "ms_per_step_device": dev_ms / k_ls, "ms_assemble": k1_ms / k_ls,
+                      "ms_lu_backsolve": k2k5_ms / k_ls,
+                      "roofline": {"bound": "tensor", "flops_per_leaf": f_ls,
+                                   "achieved": n * f_ls / (k2k5_ms / k_ls / 1e3) / 1e12, "peak": FP64_PEAK_TFLOPS,
+                                   "unit": "TFLOP/s",
+                                   "frac": n * f_ls / (k2k5_ms / k_ls / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
+                                   "note": "F_leafsolve = 2/3 n_i^3 + 2 n_i^2 + 2 n_i n_b (SURVEY 8d) over the "
+                                           "K2+K5 device time"},
+                      "h2d_bytes_per_step": int(n * (2 * p * p + nb) * 8), "d2h_bytes_per_step": int(n * p * p * 8)}
+        for a_ in (pb, pf, pv, pu):
+            a_.free()
 
     # ---- secondary: C2 (p=22, configs[1]) device-resident, same K/W ----
     secondary = None
@@ -352,10 +448,11 @@ def main():
         st2.close()
 
     # ---- CPU baseline (rank 0, N=1 only) ----
-    cpu = None
+    cpu, parity = None, None
     if world == 1 and not args.no_cpu:
-        v, cores, sample = cpu_baseline(cfg, args.cpu_seconds)
-        cpu = {"value": v, "unit": "leaves/s", "cores": cores, "kind": "port", "sample": sample}
+        v, cores, sample, parity = cpu_baseline(cfg, args.cpu_seconds, b, T_dev=d_T.cpu().numpy())
+        cpu = {"value": v, "unit": "leaves/s", "cores": cores, "kind": "port", "sample": sample,
+               "cpu_model": cpu_model()}
 
     if rank == 0:
         value = cfg["n_leaves"] * args.steps / (ms_max / 1e3)
@@ -384,12 +481,14 @@ def main():
                          "traffic_unit": "DRAM bytes per K2 launch (ncu, scaled to the launch's leaves)",
                          "k1_ms_per_step_rank0": tim["ms_assemble"] / args.steps},
             "cpu_baseline": cpu,
+            "parity": parity,
             "e2e": e2e,
             "gpu_launches": kernels,
             "clocks": clk,
             "resonant_leaves_rank0": bad,
             "chunk_leaves": info["chunk_leaves"],
             "secondary": secondary,
+            "leaf_solve": leaf_solve,
         }
         print(json.dumps(line), flush=True)
     stage.close()

@@ -24,17 +24,30 @@
 #include <vector>
 #include <stdexcept>
 
+#ifdef HPSO_REFERENCE_HEADERS
+#include <hps/errors.hpp>   // the reference's own taxonomy (proj/include/hps/errors.hpp)
+#endif
+
 namespace hpso {
 
-// Error taxonomy mirrors proj/include/hps/errors.hpp:10-26 (ParameterError is an
+// Error taxonomy: the reference's classes when its headers are on the include path,
+// else a restatement of proj/include/hps/errors.hpp:10-26 (ParameterError is an
 // invalid_argument, ResonanceError carries the element id).
+#ifdef HPSO_REFERENCE_HEADERS
+using ParameterError = hps::ParameterError;
+using ResonanceError = hps::ResonanceError;
+#else
 struct ParameterError : std::invalid_argument {
   using std::invalid_argument::invalid_argument;
 };
 struct ResonanceError : std::runtime_error {
-  int element;
-  ResonanceError(int e, const std::string& m) : std::runtime_error(m), element(e) {}
+  ResonanceError(int e, const std::string& m) : std::runtime_error(m), element_id_(e) {}
+  int element_id() const { return element_id_; }
+
+ private:
+  int element_id_;
 };
+#endif
 
 // ---- chebyshev --------------------------------------------
 // x_k = sin(pi*(2k-(p-1)) / (2(p-1))): ascending CGL nodes, exactly antisymmetric
@@ -123,8 +136,10 @@ double dirichlet_value(const MeshIndex& m, int e, int side, int k_along, const d
 // Dynamic-dispatch thread pool: every index runs on exactly one worker, so
 // per-index outputs are bitwise-independent of the worker count; the first
 // exception is rethrown after all workers join.
+#ifndef HPSO_REFERENCE_HEADERS   // else hps::hardware_workers / hps::parallel_for (.inl)
 int hardware_workers();
 template <class Fn> void parallel_for(int n, int workers, Fn&& fn);
+#endif
 
 }  // namespace hpso
 

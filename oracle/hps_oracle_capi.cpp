@@ -31,6 +31,14 @@ struct BlasInit {
 extern "C" {
 
 const char* hpso_last_error() { return g_err.c_str(); }
+// Which batching/error headers the oracle was compiled against.
+const char* hpso_build_info() {
+#ifdef HPSO_REFERENCE_HEADERS
+  return "reference headers: proj/include/hps/parallel.hpp + errors.hpp";
+#else
+  return "restated parallel.hpp/errors.hpp (reference headers absent at build time)";
+#endif
+}
 int hpso_hardware_workers() { return hpso::hardware_workers(); }
 
 int hpso_cheb_nodes(int p, int allow_small, double* x) {

@@ -1,6 +1,15 @@
-// Restatement of the reference batching contract (proj/include/hps/parallel.hpp:13-58).
+// Batching of the oracle: the reference's own proj/include/hps/parallel.hpp when it is
+// available at build time (oracle/Makefile adds -I/root/reference/proj/include and
+// -DHPSO_REFERENCE_HEADERS), else this restatement of it (parallel.hpp:13-58).
 // TEST INFRASTRUCTURE ONLY (see hps_oracle.hpp).
 #pragma once
+#ifdef HPSO_REFERENCE_HEADERS
+#include <hps/parallel.hpp>
+namespace hpso {
+using hps::hardware_workers;
+using hps::parallel_for;
+}  // namespace hpso
+#else
 #include <atomic>
 #include <exception>
 #include <mutex>
@@ -48,3 +57,4 @@ void parallel_for(int n, int workers, Fn&& fn) {
 }
 
 }  // namespace hpso
+#endif  // HPSO_REFERENCE_HEADERS

@@ -170,3 +170,11 @@ def assemble_reduced(nx, ny, p, T, w, g_bnd):
 
 def hardware_workers():
     return lib().hpso_hardware_workers()
+
+
+def build_info():
+    """Which batching/error headers the oracle was compiled against (the reference's own
+    proj/include/hps/{parallel,errors}.hpp when /root/reference was present at build time)."""
+    f = lib().hpso_build_info
+    f.restype = C.c_char_p
+    return f().decode()

@@ -243,14 +243,17 @@ class LeafStage:
         return dict(r_int2=out[0], r_flux2=out[1], f_int2=out[2])
 
     # -- leaf_solve ---------------------------------------------------------------------------
-    def leaf_solve(self, b, f, v, e0=0):
+    def leaf_solve(self, b, f, v, e0=0, out=None):
+        """Batched leaf_solve for elements [e0, e0+n): (n, p*p) local
+        solutions.  `out`: optional caller-owned (n, p*p) float64 array (pinned for overlap)."""
         pp = self.p * self.p
         b = _f64(b, (-1, pp)); f = _f64(f, (-1, pp)); v = _f64(v, (-1, self.n_b))
         n = b.shape[0]
         _rows(f, n, "f"); _rows(v, n, "v")
         if e0 < 0 or e0 + n > self.n_leaves:
             raise ParameterError(f"element range [{e0}, {e0 + n}) outside the mesh of {self.n_leaves} leaves")
-        u = np.empty((n, pp)); st = np.zeros(n, np.int32)
+        u = np.empty((n, pp)) if out is None else _out(out, (n, pp), np.float64, "out u")
+        st = np.zeros(n, np.int32)
         rc = lib().hps_gpu_leaf_solve(self._h, e0, e0 + n, _ptr(b), _ptr(f), _ptr(v), _ptr(u), _ptr(st))
         self._check(rc, st, e0)
         return u

@@ -116,3 +116,9 @@ def flops_condense(p: int) -> float:
     """F_condense(p) = 2/3 n_i^3 + 2 n_i^2 n_b + 2 n_b^2 n_i."""
     ni, nb = (p - 2) ** 2, 4 * (p - 1)
     return (2.0 / 3.0) * ni ** 3 + 2.0 * ni ** 2 * nb + 2.0 * nb ** 2 * ni
+
+
+def flops_leaf_solve(p: int) -> float:
+    """F_leafsolve(p) = 2/3 n_i^3 + 2 n_i^2 + 2 n_i n_b with the recompute policy."""
+    ni, nb = (p - 2) ** 2, 4 * (p - 1)
+    return (2.0 / 3.0) * ni ** 3 + 2.0 * ni ** 2 + 2.0 * ni * nb

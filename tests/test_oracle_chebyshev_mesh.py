@@ -135,3 +135,14 @@ def test_active_ordering_is_edge_major_by_x_then_y():
     mids = np.array(mids)
     key = np.lexsort((mids[:, 1], mids[:, 0]))
     assert np.array_equal(key, np.arange(len(mids)))
+
+
+def test_oracle_uses_reference_headers_when_present():
+    """The oracle's batching and error classes are the reference's own headers
+    (proj/include/hps/parallel.hpp, errors.hpp) whenever they exist at build time."""
+    import os
+    info = O.build_info()
+    if os.path.exists("/root/reference/proj/include/hps/parallel.hpp"):
+        assert info.startswith("reference headers"), info
+    else:
+        assert "restated" in info or info.startswith("reference headers"), info

@@ -8,7 +8,7 @@ NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-ffp-contract=off
 SRC       := paper_2211_14969_b200/csrc
 OBJDIR    := build/obj
 LIB       := paper_2211_14969_b200/_lib/libhps_leaf_b200.so
-CU        := $(SRC)/k0_fields.cu $(SRC)/k1_assemble.cu $(SRC)/k2s_small.cu $(SRC)/k4_scatter.cu $(SRC)/k5_leaf_solve.cu $(SRC)/k6_residual.cu
+CU        := $(SRC)/k0_fields.cu $(SRC)/k1_assemble.cu $(SRC)/k1_operator.cu $(SRC)/k2s_small.cu $(SRC)/k4_scatter.cu $(SRC)/k5_leaf_solve.cu $(SRC)/k6_residual.cu
 CPP       := $(SRC)/hps_host.cpp $(SRC)/hps_api.cpp
 HDRS      := $(wildcard $(SRC)/*.h $(SRC)/*.cuh include/*.h include/hps/*.hpp)
 # K2/K3 are built twice: 8-warp CTAs (g256) and 4-warp CTAs for small leaves (g128).
@@ -57,9 +57,15 @@ clean:
 CXX_TEST := build/test_leaf_api
 cxx_test: $(CXX_TEST)
 
+# Compiled against the reference's own errors.hpp (included first) when it exists.
+REF_INC   ?= /root/reference/proj/include
+ifneq ($(wildcard $(REF_INC)/hps/errors.hpp),)
+CXX_TEST_REF := -I$(REF_INC) -DHPS_TEST_REFERENCE_ERRORS
+endif
+
 $(CXX_TEST): tests/cxx/test_leaf_api.cpp include/hps/leaf_gpu.hpp include/hps_leaf_gpu.h $(LIB)
 	@mkdir -p build
-	g++ -std=c++20 -O2 -Iinclude -o $@ $< -L$(dir $(LIB)) -lhps_leaf_b200 \
+	g++ -std=c++20 -O2 -Wall -Iinclude $(CXX_TEST_REF) -o $@ $< -L$(dir $(LIB)) -lhps_leaf_b200 \
 	    -Wl,-rpath,'$$ORIGIN/../paper_2211_14969_b200/_lib'
 
 # A/B copy of the library with other K2 knobs, e.g.

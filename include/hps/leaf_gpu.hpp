@@ -3,11 +3,16 @@
 //  the reference's `leaf` and `assembly` operations).
 //
 //  Same operation names, argument meaning and error behaviour as the
-//  reference specification:
+//  reference specification, as free functions in namespace hps:
+//    build_leaf_operator(topo, spec, e)
+//    condense_leaf(ops, f_local)
 //    batched_condense(topo, spec, f)
-//    leaf_solve (batched, recipe = recompute)
+//    leaf_solve(ops-or-recipe, condensed, v, f) SPEC.md:297-305
 //    assemble_reduced(topo, leaves, spec)
-//    reconstruct_full_solution(...)             SPEC.md:363-371 (interiors via K5)
+//    reconstruct_full_solution(topo, leaves, u, spec, f)
+//  (each thread keeps one GPU context per mesh/problem shape; set_leaf_config picks the
+//  device, storage policy and worker count), and as the explicit
+//  one-context-per-GPU class hps::b200::LeafStage.
 //  Errors: hps::ParameterError (std::invalid_argument) and
 //  hps::ResonanceError(element_id) exactly as proj/include/hps/errors.hpp:10-26
 //  declares them; when that header is included first its classes are used.
@@ -15,6 +20,7 @@
 //  there is no CPU fallback — a missing GPU raises.
 // ============================================================================
 #pragma once
+#include <array>
 #include <cstdint>
 #include <functional>
 #include <memory>
@@ -104,6 +110,50 @@ struct ReducedBlocks {
   std::vector<double> blocks;  // nnzb * q * q
   std::vector<double> rhs;
 };
+
+// LeafOperators.
+struct LeafOperators {
+  int element_id = -1;
+  int p = 0;
+  std::vector<double> A_loc;                    // p^2 x p^2 row-major, local order l = iy*p + ix
+  std::vector<int> interior_idx;                // (p-2)^2 local ids, ascending
+  std::vector<int> boundary_idx;                // 4(p-1) local ids: S, E, N, W (corners on the first edge)
+  std::array<std::vector<double>, 4> D_normal;  // S, E, N, W: p x p^2 row-major, edge nodes ascending
+};
+
+// Recompute recipe of a CondensedLeaf's load_map: the element is rebuilt
+// from the mesh and the problem (element id = CondensedLeaf::element_id).
+struct LeafRecipe {
+  MeshTopology topo;
+  ProblemSpec spec;
+};
+
+// Configuration of the free functions (worker count, storage policy) plus the
+// GPU they run on.  Applies to the calling thread's contexts created afterwards.
+struct LeafConfig {
+  int device = 0;
+  StoragePolicy storage = StoragePolicy::Recompute;
+  int workers = 0;                     // host sampling threads (parallel.hpp semantics)
+  int64_t workspace_bytes = int64_t(16) << 30;   // device budget per context
+};
+void set_leaf_config(const LeafConfig& cfg);
+LeafConfig leaf_config();
+
+LeafOperators build_leaf_operator(const MeshTopology& topo, const ProblemSpec& spec, int element_id);
+CondensedLeaf condense_leaf(const LeafOperators& ops, const std::vector<double>& f_local);
+// f: full-grid load (N values), or empty to sample spec.body_load_f.  Throws ResonanceError
+// for the smallest failing element id (message lists all of them).
+std::vector<CondensedLeaf> batched_condense(const MeshTopology& topo, const ProblemSpec& spec,
+                                            const std::vector<double>& f = {});
+std::vector<double> leaf_solve(const LeafOperators& ops, const CondensedLeaf& condensed,
+                               const std::vector<double>& boundary_values, const std::vector<double>& f_local);
+std::vector<double> leaf_solve(const LeafRecipe& recipe, const CondensedLeaf& condensed,
+                               const std::vector<double>& boundary_values, const std::vector<double>& f_local);
+ReducedSystem assemble_reduced(const MeshTopology& topo, const std::vector<CondensedLeaf>& leaves,
+                               const ProblemSpec& spec);
+std::vector<double> reconstruct_full_solution(const MeshTopology& topo, const std::vector<CondensedLeaf>& leaves,
+                                              const std::vector<double>& reduced_solution,
+                                              const ProblemSpec& spec, const std::vector<double>& f = {});
 
 namespace b200 {
 

@@ -173,6 +173,27 @@ int hps_gpu_assemble_reduced_bsr_device(hps_gpu_ctx* ctx, const double* d_T, con
                                         const double* d_g_bnd, double* d_bvalues, double* d_rhs,
                                         void* stream);
 
+/* The reference's single-leaf operations on operators held as values,
+ * batched over elements [e0, e1) (ids are used in error messages only):
+ *   build_leaf_operator: from b samples (p*p per leaf) the dense
+ *     A_loc = -(D (x) I)^2 - (I (x) D)^2 - kappa^2 diag(b)  (p^2 x p^2 row-major per leaf) and
+ *     D_normal = the outward normal derivative maps of the S, E, N, W edges, each p x p^2
+ *     (edge nodes ascending, corners on both edges; 4 p p^2 per leaf).
+ *     Entries are bit-identical to the oracle's.
+ *   condense_leaf of GIVEN operators: T, w, S (nullable) and status as
+ *     hps_gpu_condense; interior/boundary blocks are gathered from A_loc, the flux rows from
+ *     D_normal (a corner uses its owning edge).
+ *   leaf_solve with a given A_loc: u (p*p per leaf) = [A_ii^{-1}(f_i -
+ *     A_ib v) on the interior, v on the boundary].
+ * Synchronous; the factors of the 'store' policy are not kept by these calls. */
+int hps_gpu_build_leaf_operator(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, double* A_loc,
+                                double* D_normal);
+int hps_gpu_condense_operator(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* A_loc,
+                              const double* D_normal, const double* f, double* T, double* w, double* S,
+                              int32_t* status);
+int hps_gpu_leaf_solve_operator(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* A_loc, const double* f,
+                                const double* v, double* u, int32_t* status);
+
 /* Test hook: zero interior row 0 of A_ii for these element
  * ids, which forces a zero pivot.  n = 0 clears. */
 int hps_gpu_set_fault_injection(hps_gpu_ctx* ctx, const int32_t* elements, int32_t n);

@@ -249,6 +249,7 @@ struct hps_gpu_ctx {
   bool no_stage = false;
   DevBuf phase_buf;
   DevBuf field_off, field_cent;   // K0 crystal sampler: node offsets, centres
+  DevBuf op_A, op_Dn, op_b, op_f, op_v, op_T, op_w, op_st, op_S, op_u;   // operator-path staging
   DevBuf res_flux, res_pl, res_pe, res_in;   // K6 residual scratch
   int store_e0 = -1, store_e1 = -1;
   HostBuf h_status;               // pinned staging of status[] (see HostBuf)
@@ -1224,6 +1225,151 @@ int hps_gpu_assemble_reduced(hps_gpu_ctx* ctx, const double* T, const double* w,
 int hps_gpu_assemble_reduced_bsr(hps_gpu_ctx* ctx, const double* T, const double* w,
                                  const double* g_bnd, double* bvalues, double* rhs) {
   return assemble_reduced_host(ctx, T, w, g_bnd, bvalues, rhs, true);
+}
+
+// ---------------------------------------------------------------------------
+// The reference's per-leaf operations on operators given as values:
+// build_leaf_operator -> (A_loc, D_normal), condense_leaf(ops, f), leaf_solve(ops, ...).
+// Synchronous, in sub-batches sized to a staging budget; K2/K3/K5 are the hot-path kernels.
+// ---------------------------------------------------------------------------
+static int op_batch(const hps_gpu_ctx* ctx, size_t bytes_per_leaf) {
+  const size_t budget = size_t(2) << 30;   // 2 GB of operator staging per sub-batch
+  return int(std::max<size_t>(1, std::min<size_t>(size_t(ctx->chunk), budget / std::max<size_t>(1, bytes_per_leaf))));
+}
+
+int hps_gpu_build_leaf_operator(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, double* A_loc,
+                                double* D_normal) {
+  if (!ctx) return HPS_ERR_PARAM;
+  if (int rc = check_range(ctx, e0, e1)) return rc;
+  if (e1 == e0) return HPS_OK;
+  if (!b || !A_loc || !D_normal) return ctx->fail(HPS_ERR_PARAM, "ParameterError: null buffer");
+  CK(cudaSetDevice(ctx->device));
+  const int p = ctx->d.p;
+  const size_t pp = size_t(p) * p, na = pp * pp, nd = 4 * size_t(p) * pp;
+  const int sub = op_batch(ctx, (na + nd + pp) * 8);
+  CK(ctx->op_A.ensure(size_t(sub) * na * 8));
+  CK(ctx->op_Dn.ensure(size_t(sub) * nd * 8));
+  CK(ctx->op_b.ensure(size_t(sub) * pp * 8));
+  cudaStream_t st = ctx->s_comp;
+  CK(cudaStreamWaitEvent(st, ctx->ev_scratch, 0));
+  for (int c0 = e0; c0 < e1; c0 += sub) {
+    const int n = std::min(sub, e1 - c0);
+    const size_t off = size_t(c0 - e0);
+    CK(cudaMemcpyAsync(ctx->op_b.ptr, b + off * pp, n * pp * 8, cudaMemcpyHostToDevice, st));
+    hpsg::launch_leaf_operator(p, ctx->Ds.as<double>(), ctx->D2.as<double>(), ctx->k2, ctx->op_b.as<double>(),
+                               ctx->op_A.as<double>(), ctx->op_Dn.as<double>(), n, st);
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(A_loc + off * na, ctx->op_A.ptr, n * na * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(D_normal + off * nd, ctx->op_Dn.ptr, n * nd * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  CK(cudaEventRecord(ctx->ev_scratch, st));
+  return HPS_OK;
+}
+
+// Shared body of condense_operator / leaf_solve_operator.
+static int operator_pass(hps_gpu_ctx* ctx, bool solve, int32_t e0, int32_t e1, const double* A_loc,
+                         const double* D_normal, const double* f, const double* v, double* T, double* w,
+                         double* S, double* u, int32_t* status) {
+  CK(cudaSetDevice(ctx->device));
+  const LeafDims d = solve ? ctx->ds : ctx->d;
+  const int p = d.p, nb = 4 * (p - 1);
+  const size_t pp = size_t(p) * p, na = pp * pp, nd = 4 * size_t(p) * pp;
+  const int sub = op_batch(ctx, (na + (solve ? 0 : nd) + 2 * pp + nb) * 8);
+  CK(ctx->op_A.ensure(size_t(sub) * na * 8));
+  if (!solve) CK(ctx->op_Dn.ensure(size_t(sub) * nd * 8));
+  CK(ctx->op_f.ensure(size_t(sub) * pp * 8));
+  CK(ctx->op_st.ensure(size_t(sub) * 4));
+  if (solve) {
+    CK(ctx->op_v.ensure(size_t(sub) * nb * 8));
+    CK(ctx->op_u.ensure(size_t(sub) * pp * 8));
+  } else {
+    CK(ctx->op_T.ensure(size_t(sub) * nb * nb * 8));
+    CK(ctx->op_w.ensure(size_t(sub) * nb * 8));
+    if (S) {
+      CK(ctx->op_S.ensure(size_t(sub) * d.ni * nb * 8));
+      CK(ctx->uinv.ensure(size_t(4 * ctx->sms) * 4096 * 8));
+    }
+  }
+  cudaStream_t st = ctx->s_comp;
+  reset_timing(ctx);
+  CK(cudaStreamWaitEvent(st, ctx->ev_scratch, 0));
+  for (int c0 = e0; c0 < e1; c0 += sub) {
+    const int n = std::min(sub, e1 - c0);
+    const size_t off = size_t(c0 - e0);
+    CK(cudaMemcpyAsync(ctx->op_A.ptr, A_loc + off * na, n * na * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->op_f.ptr, f + off * pp, n * pp * 8, cudaMemcpyHostToDevice, st));
+    if (solve) CK(cudaMemcpyAsync(ctx->op_v.ptr, v + off * nb, n * size_t(nb) * 8, cudaMemcpyHostToDevice, st));
+    else CK(cudaMemcpyAsync(ctx->op_Dn.ptr, D_normal + off * nd, n * nd * 8, cudaMemcpyHostToDevice, st));
+    const int slot = next_timing_slot(ctx);
+    cudaEventRecord(ctx->timing_event(3 * slot), st);
+    hpsg::launch_gather_operator(d, solve, ctx->op_A.as<double>(), ctx->op_Dn.as<double>(), ctx->op_f.as<double>(),
+                                 ctx->op_v.as<double>(), ctx->ws.as<double>(), ctx->norms.as<double>(), n, st);
+    cudaEventRecord(ctx->timing_event(3 * slot + 1), st);
+    hpsg::LuArgs a;
+    a.d = d;
+    a.ws = ctx->ws.as<double>();
+    a.linv = ctx->linv.as<double>();
+    a.perm = ctx->perm.as<short>();
+    a.norms = ctx->norms.as<double>();
+    a.T_out = solve ? nullptr : ctx->op_T.as<double>();
+    a.w_out = solve ? nullptr : ctx->op_w.as<double>();
+    a.status = ctx->op_st.as<int>();
+    a.minratio = nullptr;
+    a.factor = 1;
+    a.lockstep = !solve && hpsg::use_g128(d, ctx->force_cfg);
+    hpsg::launch_lu_schur(a, n, st, ctx->force_cfg);
+    ctx->tkernels += 3;
+    if (solve) {
+      hpsg::launch_backsolve(d, a.ws, a.perm, ctx->op_v.as<double>(), ctx->op_u.as<double>(), n, st);
+      ctx->tkernels += 1;
+    } else if (S) {
+      hpsg::launch_ssolve(a, ctx->op_S.as<double>(), ctx->uinv.as<double>(), n, st, ctx->force_cfg);
+      ctx->tkernels += 1;
+    }
+    cudaEventRecord(ctx->timing_event(3 * slot + 2), st);
+    CK(cudaGetLastError());
+    if (solve) {
+      CK(cudaMemcpyAsync(u + off * pp, ctx->op_u.ptr, n * pp * 8, cudaMemcpyDeviceToHost, st));
+    } else {
+      CK(cudaMemcpyAsync(T + off * nb * nb, ctx->op_T.ptr, n * size_t(nb) * nb * 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(w + off * nb, ctx->op_w.ptr, n * size_t(nb) * 8, cudaMemcpyDeviceToHost, st));
+      if (S)
+        CK(cudaMemcpyAsync(S + off * d.ni * nb, ctx->op_S.ptr, n * size_t(d.ni) * nb * 8, cudaMemcpyDeviceToHost,
+                           st));
+    }
+    CK(cudaMemcpyAsync(status + off, ctx->op_st.ptr, n * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  }
+  CK(cudaEventRecord(ctx->ev_scratch, st));
+  finish_timing(ctx);
+  // the kept factors (if any) were overwritten
+  ctx->store_e0 = ctx->store_e1 = -1;
+  std::vector<int> bad;
+  for (int i = 0; i < e1 - e0; ++i)
+    if (status[i]) bad.push_back(e0 + i);
+  if (!bad.empty()) return resonance_error(ctx, bad);
+  return HPS_OK;
+}
+
+int hps_gpu_condense_operator(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* A_loc,
+                              const double* D_normal, const double* f, double* T, double* w, double* S,
+                              int32_t* status) {
+  if (!ctx) return HPS_ERR_PARAM;
+  if (int rc = check_range(ctx, e0, e1)) return rc;
+  if (e1 == e0) return HPS_OK;
+  if (!A_loc || !D_normal || !f || !T || !w || !status)
+    return ctx->fail(HPS_ERR_PARAM, "ParameterError: null buffer");
+  return operator_pass(ctx, false, e0, e1, A_loc, D_normal, f, nullptr, T, w, S, nullptr, status);
+}
+
+int hps_gpu_leaf_solve_operator(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* A_loc, const double* f,
+                                const double* v, double* u, int32_t* status) {
+  if (!ctx) return HPS_ERR_PARAM;
+  if (int rc = check_range(ctx, e0, e1)) return rc;
+  if (e1 == e0) return HPS_OK;
+  if (!A_loc || !f || !v || !u || !status) return ctx->fail(HPS_ERR_PARAM, "ParameterError: null buffer");
+  return operator_pass(ctx, true, e0, e1, A_loc, nullptr, f, v, nullptr, nullptr, nullptr, u, status);
 }
 
 }  // extern "C"

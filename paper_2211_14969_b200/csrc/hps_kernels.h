@@ -24,6 +24,13 @@ void launch_assemble_solve(const LeafDims& d, const int* rowcode, const int* col
                            const double* f, const double* v, double* ws, double* norms,
                            const int* inject, int n_leaves, cudaStream_t st);
 
+// K1op (k1_operator.cu): dense A_loc (p^2 x p^2) + D_normal (4 x p x p^2) of a batch of leaves
+// from b, and the gather of a given operator into the K2 workspace (+ ||A_ii||_inf).
+void launch_leaf_operator(int p, const double* Ds, const double* D2, double k2, const double* b, double* A,
+                          double* Dn, int n_leaves, cudaStream_t st);
+void launch_gather_operator(const LeafDims& d, bool solve, const double* A, const double* Dn, const double* f,
+                            const double* v, double* ws, double* norms, int n_leaves, cudaStream_t st);
+
 // Store-policy leaf solve: rhs into column `col` of a kept condense workspace.
 void launch_write_rhs(const LeafDims& d, int col, const double* D2, const double* f,
                       const double* v, double* ws, int n_leaves, cudaStream_t st);

@@ -61,7 +61,8 @@ EXPORTED = ["hps_gpu_create", "hps_gpu_destroy", "hps_gpu_last_error", "hps_gpu_
             "hps_gpu_set_fault_injection", "hps_host_alloc", "hps_host_free", "hps_gpu_version",
             "hps_gpu_sample_crystal", "hps_gpu_residual", "hps_gpu_residual_device",
             "hps_gpu_reduced_bsr_pattern", "hps_gpu_assemble_reduced_bsr",
-            "hps_gpu_assemble_reduced_bsr_device", "hps_gpu_scatter_indices"]
+            "hps_gpu_assemble_reduced_bsr_device", "hps_gpu_scatter_indices",
+            "hps_gpu_build_leaf_operator", "hps_gpu_condense_operator", "hps_gpu_leaf_solve_operator"]
 
 
 def lib():
@@ -85,7 +86,9 @@ def lib():
                      "hps_gpu_get_info", "hps_gpu_get_timing", "hps_gpu_reset_timing",
                      "hps_gpu_sample_crystal", "hps_gpu_residual", "hps_gpu_residual_device",
                      "hps_gpu_reduced_bsr_pattern", "hps_gpu_assemble_reduced_bsr",
-                     "hps_gpu_assemble_reduced_bsr_device", "hps_gpu_scatter_indices"):
+                     "hps_gpu_assemble_reduced_bsr_device", "hps_gpu_scatter_indices",
+                     "hps_gpu_build_leaf_operator", "hps_gpu_condense_operator",
+                     "hps_gpu_leaf_solve_operator"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -255,6 +258,46 @@ class LeafStage:
         u = np.empty((n, pp)) if out is None else _out(out, (n, pp), np.float64, "out u")
         st = np.zeros(n, np.int32)
         rc = lib().hps_gpu_leaf_solve(self._h, e0, e0 + n, _ptr(b), _ptr(f), _ptr(v), _ptr(u), _ptr(st))
+        self._check(rc, st, e0)
+        return u
+
+    # -- the SPEC's per-leaf operations on operators held as values ----------
+    def build_leaf_operator(self, b, e0=0):
+        """build_leaf_operator for elements [e0, e0+n) from their b samples: A_loc (n, p^2, p^2)
+        and D_normal (n, 4, p, p^2) (edges S, E, N, W, edge nodes ascending)."""
+        pp = self.p * self.p
+        b = _f64(b, (-1, pp))
+        n = b.shape[0]
+        if e0 < 0 or e0 + n > self.n_leaves:
+            raise ParameterError(f"element range [{e0}, {e0 + n}) outside the mesh of {self.n_leaves} leaves")
+        A = np.empty((n, pp, pp)); Dn = np.empty((n, 4, self.p, pp))
+        self._check(lib().hps_gpu_build_leaf_operator(self._h, e0, e0 + n, _ptr(b), _ptr(A), _ptr(Dn)))
+        return A, Dn
+
+    def condense_operator(self, A, Dn, f, e0=0, want_S=False, raise_on_resonance=True):
+        """condense_leaf of given operators: (T, w, status[, S])."""
+        pp = self.p * self.p
+        A = _f64(A, (-1, pp, pp)); n = A.shape[0]
+        Dn = _rows(_f64(Dn, (-1, 4, self.p, pp)), n, "D_normal"); f = _rows(_f64(f, (-1, pp)), n, "f")
+        if e0 < 0 or e0 + n > self.n_leaves:
+            raise ParameterError(f"element range [{e0}, {e0 + n}) outside the mesh of {self.n_leaves} leaves")
+        T = np.empty((n, self.n_b, self.n_b)); w = np.empty((n, self.n_b)); st = np.zeros(n, np.int32)
+        S = np.empty((n, self.n_i, self.n_b)) if want_S else None
+        rc = lib().hps_gpu_condense_operator(self._h, e0, e0 + n, _ptr(A), _ptr(Dn), _ptr(f), _ptr(T), _ptr(w),
+                                             _ptr(S), _ptr(st))
+        if rc != HPS_OK and (rc != HPS_ERR_RESONANCE or raise_on_resonance):
+            self._check(rc, st, e0)
+        return (T, w, st, S) if want_S else (T, w, st)
+
+    def leaf_solve_operator(self, A, f, v, e0=0):
+        """leaf_solve with given A_loc: (n, p^2) local solutions."""
+        pp = self.p * self.p
+        A = _f64(A, (-1, pp, pp)); n = A.shape[0]
+        f = _rows(_f64(f, (-1, pp)), n, "f"); v = _rows(_f64(v, (-1, self.n_b)), n, "v")
+        if e0 < 0 or e0 + n > self.n_leaves:
+            raise ParameterError(f"element range [{e0}, {e0 + n}) outside the mesh of {self.n_leaves} leaves")
+        u = np.empty((n, pp)); st = np.zeros(n, np.int32)
+        rc = lib().hps_gpu_leaf_solve_operator(self._h, e0, e0 + n, _ptr(A), _ptr(f), _ptr(v), _ptr(u), _ptr(st))
         self._check(rc, st, e0)
         return u
 

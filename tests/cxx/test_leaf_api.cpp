@@ -4,10 +4,22 @@
 //      dense solve (test-only) -> reconstruct_full_solution matches J0 to 1e-6.
 //   2. ParameterError for p < 4 and a mismatched f (programming guard).
 //   3. ResonanceError carries the smallest failing element id (errors.hpp:18-26).
+//   4. The SPEC free functions: build_leaf_operator, condense_leaf,
+//      batched_condense, leaf_solve (operator and recipe), assemble_reduced,
+//      reconstruct_full_solution; condense_leaf(build_leaf_operator(e)) is bitwise the
+//      batched result, both leaf_solve forms agree bitwise, and an exception thrown by a
+//      sampling callback on a worker thread is rethrown to the caller (parallel.hpp:42-57).
+// Built with the reference's own errors.hpp included first when it is available
+// (Makefile cxx_test: -I/root/reference/proj/include -DHPS_TEST_REFERENCE_ERRORS), so
+// the API throws the reference's exception classes.
 #include <cmath>
 #include <cstdio>
+#include <stdexcept>
 #include <vector>
 
+#ifdef HPS_TEST_REFERENCE_ERRORS
+#include <hps/errors.hpp>
+#endif
 #include "hps/leaf_gpu.hpp"
 
 static std::vector<double> dense_solve(int n, const hps::ReducedSystem& r) {
@@ -32,6 +44,119 @@ static std::vector<double> dense_solve(int n, const hps::ReducedSystem& r) {
     x[i] = s / A[size_t(i) * n + i];
   }
   return x;
+}
+
+// SPEC.md:270-371 as free functions.
+static int spec_free_functions() {
+  int fails = 0;
+  hps::MeshParams mp;
+  mp.nx = 3;
+  mp.ny = 2;
+  mp.x_extent = 1.5;   // square elements of side 0.5
+  mp.p = 14;   // the blocked K1+K2 path both for batched and per-leaf condensation
+  const auto topo = hps::build_mesh(mp);
+  hps::ProblemSpec spec;
+  spec.kappa = 11.0;
+  spec.b_field = [](double x, double y) { return 0.5 + 0.4 * std::sin(7 * x) * std::cos(5 * y); };
+  spec.body_load_f = [](double x, double y) { return std::cos(3 * x + y); };
+  spec.dirichlet_g = [](double x, double y) { return x * x - y; };
+  const int p = mp.p, pp = p * p, nb = 4 * (p - 1);
+  const auto leaves = hps::batched_condense(topo, spec);
+  // build_leaf_operator invariants and condense_leaf == batched bitwise
+  for (int e : {0, 4}) {
+    const auto ops = hps::build_leaf_operator(topo, spec, e);
+    std::vector<double> xs, ys;
+    topo.element_coords(e, xs, ys);
+    double err_lin = 0.0, err_const = 0.0;
+    for (int l : ops.interior_idx) {   // A applied to a linear field: -kappa^2 b u on interior rows
+      double s1 = 0.0, s2 = 0.0;
+      for (int m = 0; m < pp; ++m) {
+        s1 += ops.A_loc[size_t(l) * pp + m] * (1.0 + 2.0 * xs[m] - 3.0 * ys[m]);
+        s2 += ops.A_loc[size_t(l) * pp + m];
+      }
+      const double b = spec.b_field(xs[l], ys[l]);
+      err_lin = std::max(err_lin, std::fabs(s1 + spec.kappa * spec.kappa * b * (1.0 + 2.0 * xs[l] - 3.0 * ys[l])));
+      err_const = std::max(err_const, std::fabs(s2 + spec.kappa * spec.kappa * b));
+    }
+    // D_normal on alpha + beta x + gamma y: S -gamma, E +beta, N +gamma, W -beta
+    const double nrm[4] = {3.0, 2.0, -3.0, -2.0};
+    double err_dn = 0.0;
+    for (int ed = 0; ed < 4; ++ed)
+      for (int t = 0; t < p; ++t) {
+        double s = 0.0;
+        for (int m = 0; m < pp; ++m) s += ops.D_normal[ed][size_t(t) * pp + m] * (1.0 + 2.0 * xs[m] - 3.0 * ys[m]);
+        err_dn = std::max(err_dn, std::fabs(s - nrm[ed]));
+      }
+    std::vector<double> fl(pp);
+    for (int l = 0; l < pp; ++l) fl[l] = spec.body_load_f(xs[l], ys[l]);
+    const auto c = hps::condense_leaf(ops, fl);
+    const bool same = c.T_flux == leaves[e].T_flux && c.w_equiv == leaves[e].w_equiv;
+    std::printf("free functions e=%d: linear %.2e const %.2e D_normal %.2e, condense_leaf==batched %s, |S|=%zu\n",
+                e, err_lin, err_const, err_dn, same ? "bitwise" : "NO", c.S_solve.size());
+    if (!(err_lin <= 1e-6 * spec.kappa * spec.kappa && err_const <= 1e-9 * pp && err_dn <= 1e-8)) {
+      std::printf("FAIL operator invariants\n");
+      ++fails;
+    }
+    if (!same || c.S_solve.size() != size_t((p - 2) * (p - 2)) * nb) { std::printf("FAIL condense_leaf\n"); ++fails; }
+    // leaf_solve: operator form == recipe form (bitwise); S_solve reproduces the f = 0 part
+    std::vector<double> v(nb);
+    for (int k = 0; k < nb; ++k) v[k] = std::sin(0.3 * k);
+    const auto u1 = hps::leaf_solve(ops, c, v, fl);
+    const auto u2 = hps::leaf_solve(hps::LeafRecipe{topo, spec}, c, v, fl);
+    const std::vector<double> zero(pp, 0.0);
+    const auto u0 = hps::leaf_solve(ops, c, v, zero);
+    double err_s = 0.0, un = 0.0;
+    for (int i = 0; i < (p - 2) * (p - 2); ++i) {
+      double s = 0.0;
+      for (int k = 0; k < nb; ++k) s += c.S_solve[size_t(i) * nb + k] * v[k];
+      err_s = std::max(err_s, std::fabs(s - u0[ops.interior_idx[i]]));
+      un = std::max(un, std::fabs(s));
+    }
+    std::printf("  leaf_solve ops==recipe %s, S_solve.v vs solve %.2e (rel)\n", u1 == u2 ? "bitwise" : "NO",
+                err_s / un);
+    if (u1 != u2 || !(err_s <= 1e-11 * un)) { std::printf("FAIL leaf_solve forms\n"); ++fails; }
+  }
+  // assemble_reduced / reconstruct_full_solution free functions == LeafStage (bitwise)
+  {
+    hps::b200::LeafStage st(topo, spec);
+    const auto lv = st.batched_condense();
+    const auto r1 = hps::assemble_reduced(topo, leaves, spec);
+    const auto r2 = st.assemble_reduced(lv);
+    const bool same = r1.values == r2.values && r1.rhs == r2.rhs && r1.col_idx == r2.col_idx;
+    std::vector<double> ua(size_t(r1.n_active));
+    for (size_t i = 0; i < ua.size(); ++i) ua[i] = std::cos(0.01 * double(i));
+    const auto f1 = hps::reconstruct_full_solution(topo, leaves, ua, spec);
+    const auto f2 = st.reconstruct_full_solution(ua);
+    std::printf("assemble_reduced free==LeafStage %s, reconstruct free==LeafStage %s\n", same ? "bitwise" : "NO",
+                f1 == f2 ? "bitwise" : "NO");
+    if (!same || f1 != f2) { std::printf("FAIL free assemble/reconstruct\n"); ++fails; }
+  }
+  // an exception in a sampling callback on a worker thread reaches the caller
+  {
+    hps::ProblemSpec bad = spec;
+    bad.b_field = [](double x, double y) -> double {
+      if (x > 0.5 && y > 0.5) throw std::domain_error("b_field: outside the model");
+      return 1.0;
+    };
+    hps::LeafConfig cfg = hps::leaf_config();
+    cfg.workers = 4;
+    hps::set_leaf_config(cfg);
+    try {
+      hps::batched_condense(topo, bad);
+      std::printf("FAIL callback exception swallowed\n");
+      ++fails;
+    } catch (const std::domain_error& e) {
+      std::printf("callback exception rethrown: %s\n", e.what());
+    }
+    cfg.workers = 0;
+    hps::set_leaf_config(cfg);
+  }
+#ifdef HPS_TEST_REFERENCE_ERRORS
+  std::printf("error classes: the reference's proj/include/hps/errors.hpp\n");
+#else
+  std::printf("error classes: restated (reference errors.hpp not on the include path)\n");
+#endif
+  return fails;
 }
 
 int main() {
@@ -108,6 +233,7 @@ int main() {
       if (e.element_id() != 6) { std::printf("FAIL element_id %d\n", e.element_id()); ++fails; }
     }
   }
+  fails += spec_free_functions();
   try {
     hps::MeshParams bad = mp;
     bad.p = 3;

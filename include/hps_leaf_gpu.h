@@ -198,6 +198,40 @@ int hps_gpu_leaf_solve_operator(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const 
  * ids, which forces a zero pivot.  n = 0 clears. */
 int hps_gpu_set_fault_injection(hps_gpu_ctx* ctx, const int32_t* elements, int32_t n);
 
+/* ---- Leaf-range sharding over the GPUs of one box (parallel.hpp:21-24;
+ * SPEC.md:291,317).  One ctx per entry of `devices` (a device may repeat), one host thread
+ * per ctx, contiguous element ranges balanced to +-1 leaf (hps_shard_range), each shard
+ * writing its disjoint leaf-major slots of the caller's host buffers.  No collective on the
+ * data path.  Results are bitwise those of a single ctx.  assemble_reduced: each shard runs
+ * K4 on the interface edges inside its range; edges cut by a shard boundary are summed on
+ * the host in K4's operation order (hps_reduced_host_edges). ---- */
+typedef struct hps_gpu_multi hps_gpu_multi;
+int hps_gpu_multi_create(const int32_t* devices, int32_t n_devices, const hps_leaf_desc* desc,
+                         hps_gpu_multi** out);
+void hps_gpu_multi_destroy(hps_gpu_multi* m);
+const char* hps_gpu_multi_last_error(const hps_gpu_multi* m);
+/* Number of shards; lo/hi (nullable, length >= shards) receive each shard's leaf range. */
+int hps_gpu_multi_shards(const hps_gpu_multi* m, int32_t* lo, int32_t* hi);
+hps_gpu_ctx* hps_gpu_multi_ctx(hps_gpu_multi* m, int32_t shard);
+int hps_gpu_multi_condense(hps_gpu_multi* m, int32_t e0, int32_t e1, const double* b, const double* f, double* T,
+                           double* w, int32_t* status);
+int hps_gpu_multi_leaf_solve(hps_gpu_multi* m, int32_t e0, int32_t e1, const double* b, const double* f,
+                             const double* v, double* u, int32_t* status);
+int hps_gpu_multi_assemble_reduced(hps_gpu_multi* m, const double* T, const double* w, const double* g_bnd,
+                                   double* values, double* rhs);
+
+/* Host-only pieces of the sharded path (no GPU involved). */
+/* Leaf range [lo, hi) of shard i of k over n leaves (sizes n/k or n/k + 1, larger first). */
+int hps_shard_range(int32_t n, int32_t k, int32_t i, int32_t* lo, int32_t* hi);
+/* Interface edges whose two elements lie on different shards (shard_lo: first leaf of each
+ * of the k shards, ascending); edges == NULL returns the count only. */
+int hps_reduced_cut_edges(int32_t p, int32_t nx, int32_t ny, const int32_t* shard_lo, int32_t k, int32_t* edges,
+                          int64_t* n_cut);
+/* K4's values/rhs of the listed edges computed on the host in K4's operation order
+ * (bit-identical), from all leaves' T and w (leaf-major) and g_bnd. */
+int hps_reduced_host_edges(int32_t p, int32_t nx, int32_t ny, const int32_t* edges, int64_t n, const double* T,
+                           const double* w, const double* g_bnd, double* values, double* rhs);
+
 /* Pinned host memory helpers. */
 void* hps_host_alloc(size_t bytes);
 void hps_host_free(void* ptr);

@@ -250,6 +250,7 @@ struct hps_gpu_ctx {
   DevBuf phase_buf;
   DevBuf field_off, field_cent;   // K0 crystal sampler: node offsets, centres
   DevBuf op_A, op_Dn, op_b, op_f, op_v, op_T, op_w, op_st, op_S, op_u;   // operator-path staging
+  DevBuf k4_T, k4_w, k4_g, k4_vals, k4_rhs, k4_list;   // assemble_reduced (host buffers), persistent
   DevBuf res_flux, res_pl, res_pe, res_in;   // K6 residual scratch
   int store_e0 = -1, store_e1 = -1;
   HostBuf h_status;               // pinned staging of status[] (see HostBuf)
@@ -1187,31 +1188,27 @@ static int assemble_reduced_host(hps_gpu_ctx* ctx, const double* T, const double
   const size_t ng = 2 * size_t(ctx->desc.nx * (d.p - 1) + 1) + 2 * size_t(ctx->desc.ny * (d.p - 1) + 1);
   const int64_t na = ctx->mesh.n_active, nnz = ctx->mesh.nnz;
   if (na == 0) return HPS_OK;
-  DevBuf dT, dw, dg, dv, dr;
-  CK(dT.ensure(nl * nb * nb * 8));
-  CK(dw.ensure(nl * nb * 8));
-  CK(dg.ensure(ng * 8));
-  CK(dv.ensure(size_t(nnz) * 8));
-  CK(dr.ensure(size_t(na) * 8));
+  CK(ctx->k4_T.ensure(nl * nb * nb * 8));
+  CK(ctx->k4_w.ensure(nl * nb * 8));
+  CK(ctx->k4_g.ensure(ng * 8));
+  CK(ctx->k4_vals.ensure(size_t(nnz) * 8));
+  CK(ctx->k4_rhs.ensure(size_t(na) * 8));
   cudaStream_t st = ctx->s_comp;
-  CK(cudaMemcpyAsync(dT.ptr, T, nl * nb * nb * 8, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(dw.ptr, w, nl * nb * 8, cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(dg.ptr, g_bnd, ng * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ctx->k4_T.ptr, T, nl * nb * nb * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ctx->k4_w.ptr, w, nl * nb * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ctx->k4_g.ptr, g_bnd, ng * 8, cudaMemcpyHostToDevice, st));
   reset_timing(ctx);
-  cudaEvent_t t0, t1;
-  CK(cudaEventCreate(&t0));
-  CK(cudaEventCreate(&t1));
+  cudaEvent_t t0 = ctx->timing_event(0), t1 = ctx->timing_event(1);
   cudaEventRecord(t0, st);
-  hpsg::launch_reduced_values(ctx->mesh_dev(), dT.as<double>(), dw.as<double>(), dg.as<double>(),
-                              dv.as<double>(), dr.as<double>(), st, bsr);
+  hpsg::launch_reduced_values(ctx->mesh_dev(), ctx->k4_T.as<double>(), ctx->k4_w.as<double>(),
+                              ctx->k4_g.as<double>(), ctx->k4_vals.as<double>(), ctx->k4_rhs.as<double>(), st,
+                              bsr);
   cudaEventRecord(t1, st);
   CK(cudaGetLastError());
-  CK(cudaMemcpyAsync(values, dv.ptr, size_t(nnz) * 8, cudaMemcpyDeviceToHost, st));
-  CK(cudaMemcpyAsync(rhs, dr.ptr, size_t(na) * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(values, ctx->k4_vals.ptr, size_t(nnz) * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(rhs, ctx->k4_rhs.ptr, size_t(na) * 8, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   cudaEventElapsedTime(&ctx->ms_scatter, t0, t1);
-  cudaEventDestroy(t0);
-  cudaEventDestroy(t1);
   ctx->tkernels = 1;
   finish_timing(ctx);
   return HPS_OK;
@@ -1370,6 +1367,348 @@ int hps_gpu_leaf_solve_operator(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const 
   if (e1 == e0) return HPS_OK;
   if (!A_loc || !f || !v || !u || !status) return ctx->fail(HPS_ERR_PARAM, "ParameterError: null buffer");
   return operator_pass(ctx, true, e0, e1, A_loc, nullptr, f, v, nullptr, nullptr, nullptr, u, status);
+}
+
+}  // extern "C"
+
+// ============================================================================
+// Leaf-range sharding across GPUs of one box (parallel.hpp:21-24,42-57;
+// SPEC.md:291,317): one ctx per device entry, one host thread per ctx, contiguous element
+// ranges balanced to +-1 leaf, each shard's outputs written into its disjoint slots of the
+// caller's buffers.  No collective: the only cross-shard data are the interface edges whose
+// two elements sit on different shards, summed on the host in the K4 order (bit-identical).
+// A device may be listed more than once (several ctxs on one GPU, e.g. for tests).
+// ============================================================================
+struct hps_gpu_multi {
+  std::vector<hps_gpu_ctx*> ctx;
+  std::vector<int> lo, hi;          // leaf range of each shard (whole mesh)
+  MeshHost mesh;
+  int p = 0, nb = 0, n_leaves = 0;
+  std::string err;
+  ~hps_gpu_multi() {
+    for (auto* c : ctx) hps_gpu_destroy(c);
+  }
+  int fail(int code, const std::string& m) {
+    err = m;
+    return code;
+  }
+};
+
+namespace {
+
+// Contiguous ranges of [e0, e1) over k shards, sizes balanced to +-1 (first shards larger).
+void split_range(int e0, int e1, int k, std::vector<int>& lo, std::vector<int>& hi) {
+  const int n = e1 - e0, base = n / k, rem = n % k;
+  lo.assign(k, 0);
+  hi.assign(k, 0);
+  int a = e0;
+  for (int i = 0; i < k; ++i) {
+    lo[i] = a;
+    a += base + (i < rem ? 1 : 0);
+    hi[i] = a;
+  }
+}
+
+// Runs fn(i) for every shard on its own thread (serially when threads cannot be started);
+// returns the first nonzero return code in shard order.
+template <class Fn>
+std::vector<int> for_shards(int k, Fn&& fn) {
+  std::vector<int> rc(k, HPS_OK);
+  std::vector<std::thread> th;
+  int started = 0;
+  try {
+    for (int i = 1; i < k; ++i, ++started) th.emplace_back([&, i] { rc[i] = fn(i); });
+  } catch (...) {
+  }
+  if (k > 0) rc[0] = fn(0);
+  for (int i = 1 + started; i < k; ++i) rc[i] = fn(i);
+  for (auto& t : th) t.join();
+  return rc;
+}
+
+// K4's entry arithmetic for one interface edge on the host (k4_values_kernel, same IEEE
+// sequence: v = (0 + T_e0) + T_e1 over present terms; rhs = -((0 + w + sum T g) + ...)).
+void host_edge_values(const MeshHost& m, const double* T, const double* w, const double* g_bnd, int ed,
+                      double* values, double* rhs) {
+  const int p = m.p, q = p - 2, nb = 4 * (p - 1);
+  auto side_base = [p](int side) { return side == 0 ? 1 : side == 1 ? p : side == 2 ? 2 * p : 3 * p - 2; };
+  const int ne = m.edge_ne[ed];
+  const int64_t off = m.edge_off[ed];
+  const int rowlen = ne * q;
+  int el[2], sd[2], col_side[2][7];
+  for (int t = 0; t < 2; ++t) {
+    el[t] = m.edge_elems[2 * ed + t];
+    sd[t] = m.edge_sides[2 * ed + t];
+    for (int r = 0; r < 7; ++r) {
+      col_side[t][r] = -1;
+      if (r < ne)
+        for (int s4 = 0; s4 < 4; ++s4)
+          if (m.elem_edges[size_t(4) * el[t] + s4] == m.edge_cols[size_t(7) * ed + r]) col_side[t][r] = s4;
+    }
+  }
+  for (int k = 0; k < q; ++k)
+    for (int pos = 0; pos < rowlen; ++pos) {
+      const int rank = pos / q, kk = pos - rank * q;
+      double v = 0.0;
+      for (int t = 0; t < 2; ++t) {
+        const int sc = col_side[t][rank];
+        if (sc < 0) continue;
+        const int r = side_base(sd[t]) + k;
+        v = v + T[(size_t(el[t]) * nb + r) * nb + side_base(sc) + kk];
+      }
+      values[off + int64_t(k) * rowlen + pos] = v;
+    }
+  const int Nx = m.nx * (p - 1) + 1, Ny = m.ny * (p - 1) + 1;
+  for (int k = 0; k < q; ++k) {
+    double acc = 0.0;
+    for (int t = 0; t < 2; ++t) {
+      const int e = el[t];
+      const int r = side_base(sd[t]) + k;
+      const double* Te = T + (size_t(e) * nb + r) * nb;
+      acc = acc + w[size_t(e) * nb + r];
+      const int ex = e % m.nx, ey = e / m.nx;
+      for (int sc = 0; sc < 4; ++sc) {
+        if (m.elem_edges[size_t(4) * e + sc] >= 0) continue;
+        const double* gs;
+        int base;
+        switch (sc) {
+          case 0: gs = g_bnd; base = ex * (p - 1); break;
+          case 1: gs = g_bnd + 2 * Nx + Ny; base = ey * (p - 1); break;
+          case 2: gs = g_bnd + Nx; base = ex * (p - 1); break;
+          default: gs = g_bnd + 2 * Nx; base = ey * (p - 1); break;
+        }
+        for (int kk = 0; kk < q; ++kk) {
+          const double prod = Te[side_base(sc) + kk] * gs[base + kk + 1];
+          acc = acc + prod;
+        }
+      }
+    }
+    rhs[int64_t(ed) * q + k] = -acc;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+// ---- host-only pieces of the sharded path (no GPU needed) ----
+int hps_shard_range(int32_t n, int32_t k, int32_t i, int32_t* lo, int32_t* hi) {
+  if (n < 0 || k < 1 || i < 0 || i >= k || !lo || !hi) return HPS_ERR_PARAM;
+  std::vector<int> L, H;
+  split_range(0, n, k, L, H);
+  *lo = L[i];
+  *hi = H[i];
+  return HPS_OK;
+}
+
+int hps_reduced_cut_edges(int32_t p, int32_t nx, int32_t ny, const int32_t* shard_lo, int32_t k, int32_t* edges,
+                          int64_t* n_cut) {
+  if (p < 4 || nx < 1 || ny < 1 || k < 1 || !shard_lo || !n_cut) return HPS_ERR_PARAM;
+  const MeshHost mh = mesh_tables(nx, ny, p);
+  auto shard = [&](int e) {
+    int s = 0;
+    while (s + 1 < k && e >= shard_lo[s + 1]) ++s;
+    return s;
+  };
+  int64_t c = 0;
+  for (int ed = 0; ed < mh.n_edges; ++ed)
+    if (shard(mh.edge_elems[2 * ed]) != shard(mh.edge_elems[2 * ed + 1])) {
+      if (edges) edges[c] = ed;
+      ++c;
+    }
+  *n_cut = c;
+  return HPS_OK;
+}
+
+int hps_reduced_host_edges(int32_t p, int32_t nx, int32_t ny, const int32_t* edges, int64_t n, const double* T,
+                           const double* w, const double* g_bnd, double* values, double* rhs) {
+  if (p < 4 || nx < 1 || ny < 1 || (n > 0 && (!edges || !T || !w || !g_bnd || !values || !rhs)))
+    return HPS_ERR_PARAM;
+  const MeshHost mh = mesh_tables(nx, ny, p);
+  for (int64_t i = 0; i < n; ++i) {
+    if (edges[i] < 0 || edges[i] >= mh.n_edges) return HPS_ERR_PARAM;
+    host_edge_values(mh, T, w, g_bnd, edges[i], values, rhs);
+  }
+  return HPS_OK;
+}
+
+int hps_gpu_multi_create(const int32_t* devices, int32_t n_devices, const hps_leaf_desc* desc,
+                         hps_gpu_multi** out) {
+  if (!out || !desc || !devices || n_devices < 1) {
+    g_create_error = "ParameterError: hps_gpu_multi_create needs >= 1 device and a descriptor";
+    return HPS_ERR_PARAM;
+  }
+  *out = nullptr;
+  auto m = std::make_unique<hps_gpu_multi>();
+  const int n = desc->nx * desc->ny;
+  const int k = std::min<int>(n_devices, std::max(1, n));
+  m->ctx.assign(k, nullptr);
+  split_range(0, n, k, m->lo, m->hi);
+  // each ctx budgets for its own shard (the shard decides chunking; ctxs on one device
+  // share its memory, so the default budget is split between them)
+  std::vector<int> per_dev(k, 0);
+  for (int i = 0; i < k; ++i)
+    for (int j = 0; j < k; ++j) per_dev[i] += devices[j] == devices[i];
+  std::vector<std::string> errs(k);
+  for (int i = 0; i < k; ++i) {   // sequential: cudaMemGetInfo-based budgets see earlier ctxs
+    hps_leaf_desc d = *desc;
+    if (d.workspace_bytes == 0 && per_dev[i] > 1) {
+      size_t fr = 0, tot = 0;
+      cudaSetDevice(devices[i]);
+      cudaMemGetInfo(&fr, &tot);
+      const int remaining = [&] { int c = 0; for (int j = i; j < k; ++j) c += devices[j] == devices[i]; return c; }();
+      d.workspace_bytes = int64_t(double(fr) * 0.7 / remaining);
+    }
+    const int rc = hps_gpu_create(devices[i], &d, &m->ctx[i]);
+    if (rc != HPS_OK) {
+      g_create_error = "shard " + std::to_string(i) + " (device " + std::to_string(devices[i]) + "): " +
+                       g_create_error;
+      return rc;
+    }
+  }
+  m->mesh = mesh_tables(desc->nx, desc->ny, desc->p);
+  m->p = desc->p;
+  m->nb = 4 * (desc->p - 1);
+  m->n_leaves = n;
+  *out = m.release();
+  return HPS_OK;
+}
+
+void hps_gpu_multi_destroy(hps_gpu_multi* m) { delete m; }
+
+const char* hps_gpu_multi_last_error(const hps_gpu_multi* m) { return m ? m->err.c_str() : g_create_error.c_str(); }
+
+int hps_gpu_multi_shards(const hps_gpu_multi* m, int32_t* lo, int32_t* hi) {
+  if (!m) return HPS_ERR_PARAM;
+  const int k = int(m->ctx.size());
+  for (int i = 0; i < k && lo && hi; ++i) {
+    lo[i] = m->lo[i];
+    hi[i] = m->hi[i];
+  }
+  return k;
+}
+
+hps_gpu_ctx* hps_gpu_multi_ctx(hps_gpu_multi* m, int32_t shard) {
+  if (!m || shard < 0 || shard >= int(m->ctx.size())) return nullptr;
+  return m->ctx[shard];
+}
+
+// Resonance ids of all shards (status of the whole range) -> one message; other errors:
+// the first failing shard's message.
+static int multi_result(hps_gpu_multi* m, const std::vector<int>& rc, const int32_t* status, int e0, int e1) {
+  for (size_t i = 0; i < rc.size(); ++i)
+    if (rc[i] != HPS_OK && rc[i] != HPS_ERR_RESONANCE)
+      return m->fail(rc[i], "shard " + std::to_string(i) + ": " + m->ctx[i]->err);
+  std::vector<int> bad;
+  for (int i = 0; status && i < e1 - e0; ++i)
+    if (status[i]) bad.push_back(e0 + i);
+  if (bad.empty()) return HPS_OK;
+  return m->fail(HPS_ERR_RESONANCE,
+                 "ResonanceError: element " + std::to_string(bad.front()) +
+                     ": interior block singular (pivot < 1e-12*||A_ii||_inf); failing elements [" + id_list(bad) +
+                     "]");
+}
+
+int hps_gpu_multi_condense(hps_gpu_multi* m, int32_t e0, int32_t e1, const double* b, const double* f, double* T,
+                           double* w, int32_t* status) {
+  if (!m) return HPS_ERR_PARAM;
+  if (e0 < 0 || e1 > m->n_leaves || e0 > e1)
+    return m->fail(HPS_ERR_PARAM, "ParameterError: element range outside the mesh");
+  if (!b || !f || !T || !w || !status) return m->fail(HPS_ERR_PARAM, "ParameterError: null buffer");
+  const int k = int(m->ctx.size());
+  std::vector<int> lo, hi;
+  split_range(e0, e1, k, lo, hi);
+  const size_t pp = size_t(m->p) * m->p, nb = size_t(m->nb);
+  const auto rc = for_shards(k, [&](int i) {
+    const size_t o = size_t(lo[i] - e0);
+    if (hi[i] == lo[i]) return int(HPS_OK);
+    return hps_gpu_condense(m->ctx[i], lo[i], hi[i], b + o * pp, f + o * pp, T + o * nb * nb, w + o * nb, nullptr,
+                            status + o);
+  });
+  return multi_result(m, rc, status, e0, e1);
+}
+
+int hps_gpu_multi_leaf_solve(hps_gpu_multi* m, int32_t e0, int32_t e1, const double* b, const double* f,
+                             const double* v, double* u, int32_t* status) {
+  if (!m) return HPS_ERR_PARAM;
+  if (e0 < 0 || e1 > m->n_leaves || e0 > e1)
+    return m->fail(HPS_ERR_PARAM, "ParameterError: element range outside the mesh");
+  if (!b || !f || !v || !u || !status) return m->fail(HPS_ERR_PARAM, "ParameterError: null buffer");
+  const int k = int(m->ctx.size());
+  std::vector<int> lo, hi;
+  split_range(e0, e1, k, lo, hi);
+  const size_t pp = size_t(m->p) * m->p, nb = size_t(m->nb);
+  const auto rc = for_shards(k, [&](int i) {
+    const size_t o = size_t(lo[i] - e0);
+    if (hi[i] == lo[i]) return int(HPS_OK);
+    return hps_gpu_leaf_solve(m->ctx[i], lo[i], hi[i], b + o * pp, f + o * pp, v + o * nb, u + o * pp, status + o);
+  });
+  return multi_result(m, rc, status, e0, e1);
+}
+
+// assemble_reduced over shards: shard i runs K4 on the interface edges whose two elements
+// both lie in its leaf range (its T/w slice on its device), copying those edges' CSR rows
+// back; edges cut by a shard boundary are summed on the host in K4's order.
+int hps_gpu_multi_assemble_reduced(hps_gpu_multi* m, const double* T, const double* w, const double* g_bnd,
+                                   double* values, double* rhs) {
+  if (!m) return HPS_ERR_PARAM;
+  if (!T || !w || !g_bnd || !values || !rhs) return m->fail(HPS_ERR_PARAM, "ParameterError: null buffer");
+  const MeshHost& mh = m->mesh;
+  if (mh.n_active == 0) return HPS_OK;
+  const int k = int(m->ctx.size()), q = m->p - 2;
+  const size_t nb = size_t(m->nb);
+  std::vector<int> shard_of(m->n_leaves);
+  for (int i = 0; i < k; ++i)
+    for (int e = m->lo[i]; e < m->hi[i]; ++e) shard_of[e] = i;
+  std::vector<std::vector<int>> own(k);
+  std::vector<int> cut;
+  for (int ed = 0; ed < mh.n_edges; ++ed) {
+    const int s0 = shard_of[mh.edge_elems[2 * ed]], s1 = shard_of[mh.edge_elems[2 * ed + 1]];
+    if (s0 == s1) own[s0].push_back(ed);
+    else cut.push_back(ed);
+  }
+  const size_t ng = 2 * size_t(mh.nx * (m->p - 1) + 1) + 2 * size_t(mh.ny * (m->p - 1) + 1);
+  const auto rc = for_shards(k, [&](int i) -> int {
+    hps_gpu_ctx* ctx = m->ctx[i];
+    if (own[i].empty()) return HPS_OK;
+    CK(cudaSetDevice(ctx->device));
+    const size_t n = size_t(m->hi[i] - m->lo[i]);
+    CK(ctx->k4_T.ensure(n * nb * nb * 8));
+    CK(ctx->k4_w.ensure(n * nb * 8));
+    CK(ctx->k4_g.ensure(ng * 8));
+    CK(ctx->k4_vals.ensure(size_t(mh.nnz) * 8));
+    CK(ctx->k4_rhs.ensure(size_t(mh.n_active) * 8));
+    CK(ctx->k4_list.ensure(own[i].size() * 4));
+    cudaStream_t st = ctx->s_comp;
+    const size_t lo = size_t(m->lo[i]);
+    CK(cudaMemcpyAsync(ctx->k4_T.ptr, T + lo * nb * nb, n * nb * nb * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->k4_w.ptr, w + lo * nb, n * nb * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->k4_g.ptr, g_bnd, ng * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->k4_list.ptr, own[i].data(), own[i].size() * 4, cudaMemcpyHostToDevice, st));
+    // T/w of element e live at (e - lo): shift the base pointers (only own-edge elements are read)
+    hpsg::launch_reduced_values(ctx->mesh_dev(), ctx->k4_T.as<double>() - lo * nb * nb,
+                                ctx->k4_w.as<double>() - lo * nb, ctx->k4_g.as<double>(), ctx->k4_vals.as<double>(),
+                                ctx->k4_rhs.as<double>(), st, false, ctx->k4_list.as<int>(), int(own[i].size()));
+    CK(cudaGetLastError());
+    // copy back maximal runs of consecutive own edges (CSR rows of consecutive edges are contiguous)
+    const auto& L = own[i];
+    for (size_t a = 0; a < L.size();) {
+      size_t b2 = a + 1;
+      while (b2 < L.size() && L[b2] == L[b2 - 1] + 1) ++b2;
+      const int ea = L[a], eb = L[b2 - 1] + 1;
+      const int64_t v0 = mh.edge_off[ea], v1 = mh.edge_off[eb];
+      CK(cudaMemcpyAsync(values + v0, ctx->k4_vals.as<double>() + v0, size_t(v1 - v0) * 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(rhs + int64_t(ea) * q, ctx->k4_rhs.as<double>() + int64_t(ea) * q, size_t(eb - ea) * q * 8,
+                         cudaMemcpyDeviceToHost, st));
+      a = b2;
+    }
+    CK(cudaStreamSynchronize(st));
+    return HPS_OK;
+  });
+  for (int ed : cut) host_edge_values(mh, T, w, g_bnd, ed, values, rhs);
+  for (int i = 0; i < k; ++i)
+    if (rc[i] != HPS_OK) return m->fail(rc[i], "shard " + std::to_string(i) + ": " + m->ctx[i]->err);
+  return HPS_OK;
 }
 
 }  // extern "C"

@@ -127,8 +127,10 @@ struct MeshDev {
 };
 void launch_reduced_pattern(const MeshDev& m, int64_t* row_ptr, int32_t* col_idx, cudaStream_t st);
 // bsr: values in BSR layout (block row = interface edge, q x q row-major blocks).
+// edge_list (device, n_list ids): only those edges (a leaf-range shard's own edges).
 void launch_reduced_values(const MeshDev& m, const double* T, const double* w, const double* g_bnd,
-                           double* values, double* rhs, cudaStream_t st, bool bsr = false);
+                           double* values, double* rhs, cudaStream_t st, bool bsr = false,
+                           const int* edge_list = nullptr, int n_list = 0);
 void launch_reduced_bsr_pattern(const MeshDev& m, int64_t* brow_ptr, int32_t* bcol_idx, cudaStream_t st);
 // Per-leaf scatter map for leaves [e0, e0+n): slot (n x nb x nb) into the CSR values, row (n x nb).
 void launch_scatter_indices(const MeshDev& m, int e0, int n, int64_t* slot, int64_t* row, cudaStream_t st);

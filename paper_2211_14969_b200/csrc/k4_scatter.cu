@@ -65,14 +65,17 @@ __global__ void __launch_bounds__(256) k4_bsr_pattern_kernel(MeshDev m, int64_t*
   if (threadIdx.x < ne) bcol_idx[boff + threadIdx.x] = m.edge_cols[ed * 7 + threadIdx.x];
 }
 
-// grid = n_edges, block 256.  BSR selects the output layout (see the header).
+// grid = n_edges (or the length of edge_list: a leaf-range shard's own edges), block 256.
+// BSR selects the output layout (see the header).  T and w are indexed by global element
+// id (a shard passes base pointers offset by its first leaf).
 template <bool BSR>
 __global__ void __launch_bounds__(256) k4_values_kernel(MeshDev m, const double* __restrict__ T,
                                                         const double* __restrict__ w,
                                                         const double* __restrict__ g_bnd,
                                                         double* __restrict__ values,
-                                                        double* __restrict__ rhs) {
-  const int ed = blockIdx.x;
+                                                        double* __restrict__ rhs,
+                                                        const int* __restrict__ edge_list) {
+  const int ed = edge_list ? edge_list[blockIdx.x] : blockIdx.x;
   const int p = m.p, q = p - 2, nb = 4 * (p - 1);
   const int ne = m.edge_ne[ed];
   const int64_t off = m.edge_off[ed];
@@ -235,12 +238,14 @@ void launch_reduced_bsr_pattern(const MeshDev& m, int64_t* brow_ptr, int32_t* bc
 }
 
 void launch_reduced_values(const MeshDev& m, const double* T, const double* w, const double* g_bnd,
-                           double* values, double* rhs, cudaStream_t st, bool bsr) {
-  if (m.n_edges <= 0) return;
+                           double* values, double* rhs, cudaStream_t st, bool bsr, const int* edge_list,
+                           int n_list) {
+  const int grid = edge_list ? n_list : m.n_edges;
+  if (grid <= 0) return;
   if (bsr)
-    k4_values_kernel<true><<<m.n_edges, 256, 0, st>>>(m, T, w, g_bnd, values, rhs);
+    k4_values_kernel<true><<<grid, 256, 0, st>>>(m, T, w, g_bnd, values, rhs, edge_list);
   else
-    k4_values_kernel<false><<<m.n_edges, 256, 0, st>>>(m, T, w, g_bnd, values, rhs);
+    k4_values_kernel<false><<<grid, 256, 0, st>>>(m, T, w, g_bnd, values, rhs, edge_list);
 }
 
 void launch_scatter_indices(const MeshDev& m, int e0, int n, int64_t* slot, int64_t* row, cudaStream_t st) {

@@ -62,7 +62,11 @@ EXPORTED = ["hps_gpu_create", "hps_gpu_destroy", "hps_gpu_last_error", "hps_gpu_
             "hps_gpu_sample_crystal", "hps_gpu_residual", "hps_gpu_residual_device",
             "hps_gpu_reduced_bsr_pattern", "hps_gpu_assemble_reduced_bsr",
             "hps_gpu_assemble_reduced_bsr_device", "hps_gpu_scatter_indices",
-            "hps_gpu_build_leaf_operator", "hps_gpu_condense_operator", "hps_gpu_leaf_solve_operator"]
+            "hps_gpu_build_leaf_operator", "hps_gpu_condense_operator", "hps_gpu_leaf_solve_operator",
+            "hps_gpu_multi_create", "hps_gpu_multi_destroy", "hps_gpu_multi_last_error", "hps_gpu_multi_shards",
+            "hps_gpu_multi_ctx", "hps_gpu_multi_condense", "hps_gpu_multi_leaf_solve",
+            "hps_gpu_multi_assemble_reduced", "hps_shard_range", "hps_reduced_cut_edges",
+            "hps_reduced_host_edges"]
 
 
 def lib():
@@ -80,6 +84,11 @@ def lib():
         L.hps_host_alloc.restype = C.c_void_p
         L.hps_host_alloc.argtypes = [C.c_size_t]
         L.hps_host_free.argtypes = [C.c_void_p]
+        L.hps_gpu_multi_last_error.restype = C.c_char_p
+        L.hps_gpu_multi_last_error.argtypes = [C.c_void_p]
+        L.hps_gpu_multi_create.argtypes = [C.c_void_p, C.c_int32, C.POINTER(_Desc), C.POINTER(C.c_void_p)]
+        L.hps_gpu_multi_destroy.argtypes = [C.c_void_p]
+        L.hps_gpu_multi_ctx.restype = C.c_void_p
         for name in ("hps_gpu_condense", "hps_gpu_condense_device", "hps_gpu_leaf_solve",
                      "hps_gpu_reduced_pattern", "hps_gpu_assemble_reduced",
                      "hps_gpu_assemble_reduced_device", "hps_gpu_set_fault_injection",
@@ -88,7 +97,9 @@ def lib():
                      "hps_gpu_reduced_bsr_pattern", "hps_gpu_assemble_reduced_bsr",
                      "hps_gpu_assemble_reduced_bsr_device", "hps_gpu_scatter_indices",
                      "hps_gpu_build_leaf_operator", "hps_gpu_condense_operator",
-                     "hps_gpu_leaf_solve_operator"):
+                     "hps_gpu_leaf_solve_operator", "hps_gpu_multi_shards", "hps_gpu_multi_condense",
+                     "hps_gpu_multi_leaf_solve", "hps_gpu_multi_assemble_reduced", "hps_shard_range",
+                     "hps_reduced_cut_edges", "hps_reduced_host_edges"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -352,6 +363,133 @@ class LeafStage:
         vals = np.empty((ci.size, q, q)); rhs = np.empty((rp.size - 1) * q)
         self._check(lib().hps_gpu_assemble_reduced_bsr(self._h, _ptr(T), _ptr(w), _ptr(g_bnd), _ptr(vals), _ptr(rhs)))
         return rp, ci, vals, rhs
+
+
+def shard_range(n, k, i):
+    """Leaf range [lo, hi) of shard i of k (hps_shard_range: contiguous, balanced to +-1)."""
+    lo, hi = C.c_int32(), C.c_int32()
+    if lib().hps_shard_range(n, k, i, C.byref(lo), C.byref(hi)) != HPS_OK:
+        raise ParameterError(f"shard_range({n}, {k}, {i})")
+    return lo.value, hi.value
+
+
+def reduced_cut_edges(p, nx, ny, shard_lo):
+    """Interface edges whose two elements lie on different shards (host only)."""
+    lo = np.ascontiguousarray(shard_lo, np.int32)
+    n = C.c_int64()
+    if lib().hps_reduced_cut_edges(p, nx, ny, _ptr(lo), lo.size, None, C.byref(n)) != HPS_OK:
+        raise ParameterError("reduced_cut_edges")
+    out = np.empty(max(n.value, 1), np.int32)
+    lib().hps_reduced_cut_edges(p, nx, ny, _ptr(lo), lo.size, _ptr(out), C.byref(n))
+    return out[:n.value]
+
+
+def reduced_host_edges(p, nx, ny, edges, T, w, g_bnd, values, rhs):
+    """K4's values/rhs of `edges` on the host, in K4's operation order, into the CSR arrays
+    values/rhs (modified in place)."""
+    e = np.ascontiguousarray(edges, np.int32)
+    T = _f64(T); w = _f64(w); g_bnd = _f64(g_bnd)
+    _out(values, values.shape, np.float64, "values"); _out(rhs, rhs.shape, np.float64, "rhs")
+    if lib().hps_reduced_host_edges(p, nx, ny, _ptr(e), e.size, _ptr(T), _ptr(w), _ptr(g_bnd), _ptr(values),
+                                    _ptr(rhs)) != HPS_OK:
+        raise ParameterError("reduced_host_edges")
+
+
+class MultiLeafStage:
+    """Leaf-range sharding of one mesh over several GPU contexts (hps_gpu_multi_*): one host
+    thread per ctx, contiguous +-1-balanced ranges, no collective; bitwise equal to a single
+    LeafStage.  `devices` may repeat a GPU (several ctxs on one device)."""
+
+    def __init__(self, p, nx, ny, kappa, devices, a=None, storage=STORAGE_RECOMPUTE, workspace_bytes=0):
+        L = lib()
+        d = _Desc(p=p, nx=nx, ny=ny, storage=storage, a=(1.0 / nx if a is None else a),
+                  kappa=kappa, workspace_bytes=int(workspace_bytes))
+        dv = np.ascontiguousarray(devices, np.int32)
+        h = C.c_void_p()
+        rc = L.hps_gpu_multi_create(_ptr(dv), dv.size, C.byref(d), C.byref(h))
+        if rc != HPS_OK:
+            msg = L.hps_gpu_multi_last_error(None).decode()
+            raise (ParameterError if rc == HPS_ERR_PARAM else CudaError)(msg)
+        self._h = h
+        self.p, self.nx, self.ny, self.kappa = p, nx, ny, kappa
+        self.n_leaves = nx * ny
+        self.n_i, self.n_b = (p - 2) ** 2, 4 * (p - 1)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hps_gpu_multi_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def _check(self, rc, status=None, e0=0):
+        if rc == HPS_OK:
+            return
+        msg = lib().hps_gpu_multi_last_error(self._h).decode()
+        if rc == HPS_ERR_RESONANCE:
+            failing = [] if status is None else [e0 + int(i) for i in np.nonzero(status)[0]]
+            raise ResonanceError(failing[0] if failing else -1, msg, failing)
+        if rc == HPS_ERR_PARAM:
+            raise ParameterError(msg)
+        raise CudaError(msg)
+
+    def shards(self):
+        k = lib().hps_gpu_multi_shards(self._h, None, None)
+        lo = np.empty(k, np.int32); hi = np.empty(k, np.int32)
+        lib().hps_gpu_multi_shards(self._h, _ptr(lo), _ptr(hi))
+        return list(zip(lo.tolist(), hi.tolist()))
+
+    def condense(self, b, f, e0=0, out=None, raise_on_resonance=True):
+        pp = self.p * self.p
+        b = _f64(b, (-1, pp)); f = _rows(_f64(f, (-1, pp)), b.shape[0], "f")
+        n = b.shape[0]
+        if out is None:
+            T = np.empty((n, self.n_b, self.n_b)); w = np.empty((n, self.n_b))
+        else:
+            T = _out(out[0], (n, self.n_b, self.n_b), np.float64, "out T")
+            w = _out(out[1], (n, self.n_b), np.float64, "out w")
+        st = np.zeros(n, np.int32)
+        rc = lib().hps_gpu_multi_condense(self._h, e0, e0 + n, _ptr(b), _ptr(f), _ptr(T), _ptr(w), _ptr(st))
+        if rc != HPS_OK and (rc != HPS_ERR_RESONANCE or raise_on_resonance):
+            self._check(rc, st, e0)
+        return T, w, st
+
+    def leaf_solve(self, b, f, v, e0=0):
+        pp = self.p * self.p
+        b = _f64(b, (-1, pp)); n = b.shape[0]
+        f = _rows(_f64(f, (-1, pp)), n, "f"); v = _rows(_f64(v, (-1, self.n_b)), n, "v")
+        u = np.empty((n, pp)); st = np.zeros(n, np.int32)
+        rc = lib().hps_gpu_multi_leaf_solve(self._h, e0, e0 + n, _ptr(b), _ptr(f), _ptr(v), _ptr(u), _ptr(st))
+        self._check(rc, st, e0)
+        return u
+
+    def assemble_reduced(self, T, w, g_bnd, pattern_from=None):
+        """(row_ptr, col_idx, values, rhs); the pattern comes from shard 0's context."""
+        ctx = lib().hps_gpu_multi_ctx(self._h, 0)
+        nnz = C.c_int64()
+        lib().hps_gpu_reduced_pattern(C.c_void_p(ctx), C.byref(nnz), None, None)
+        i = _Info()
+        lib().hps_gpu_get_info(C.c_void_p(ctx), C.byref(i))
+        na = i.n_active
+        rp = np.empty(na + 1, np.int64); ci = np.empty(max(nnz.value, 1), np.int32)
+        lib().hps_gpu_reduced_pattern(C.c_void_p(ctx), C.byref(nnz), _ptr(rp), _ptr(ci))
+        T = _rows(_f64(T, (-1, self.n_b, self.n_b)), self.n_leaves, "T")
+        w = _rows(_f64(w, (-1, self.n_b)), self.n_leaves, "w")
+        g_bnd = _f64(g_bnd, (-1,))
+        vals = np.empty(nnz.value); rhs = np.empty(na)
+        self._check(lib().hps_gpu_multi_assemble_reduced(self._h, _ptr(T), _ptr(w), _ptr(g_bnd), _ptr(vals),
+                                                         _ptr(rhs)))
+        return rp, ci[:nnz.value], vals, rhs
 
 
 class _PinnedOwner:

@@ -99,6 +99,14 @@ int hps_gpu_reset_timing(hps_gpu_ctx* ctx);
 int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, const double* f,
                      double* T, double* w, double* S, int32_t* status);
 
+/* batched_condense + assemble_reduced of the whole mesh with the
+ * leaves' T/w kept resident in HBM: b, f are all n_leaves leaves' samples (host), g_bnd the
+ * Dirichlet samples (layout of hps_gpu_assemble_reduced); the host receives the CSR values
+ * (pattern: hps_gpu_reduced_pattern) and rhs, bit-identical to condense + assemble_reduced,
+ * plus T/w when both are non-null.  T never round-trips through the host for K4. */
+int hps_gpu_condense_assemble(hps_gpu_ctx* ctx, const double* b, const double* f, const double* g_bnd,
+                              double* values, double* rhs, double* T, double* w, int32_t* status);
+
 /* Same operation on device-resident buffers (inputs already in HBM, outputs
  * stay in HBM), enqueued on `stream` (cudaStream_t, NULL = ctx stream). */
 int hps_gpu_condense_device(hps_gpu_ctx* ctx, int32_t e0, int32_t n, const double* d_b,

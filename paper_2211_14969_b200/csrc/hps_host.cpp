@@ -764,11 +764,11 @@ static bool host_pinned(const void* ptr) {
   return at.type == cudaMemoryTypeHost;
 }
 
-int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, const double* f,
-                     double* T, double* w, double* S, int32_t* status) {
-  if (!ctx) return HPS_ERR_PARAM;
-  if (int rc = check_range(ctx, e0, e1)) return rc;
-  if (!b || !f || !T || !w || !status) return ctx->fail(HPS_ERR_PARAM, "ParameterError: null buffer");
+// Host-buffer condense pipeline.  dT_res/dw_res (device, nullable): keep every leaf's T/w
+// resident in HBM at (e - e0) instead of the double-buffered staging (hps_gpu_condense_assemble
+// runs K4 on them afterwards); T/w (host) may then be null (no D2H of T at all).
+static int condense_pipeline(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, const double* f,
+                             double* T, double* w, double* S, int32_t* status, double* dT_res, double* dw_res) {
   if (ctx->desc.storage == HPS_STORAGE_STORE && (e1 - e0) > ctx->chunk)
     return ctx->fail(HPS_ERR_PARAM, "ParameterError: store policy range exceeds resident factors");
   CK(cudaSetDevice(ctx->device));
@@ -778,8 +778,10 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
   for (int i = 0; i < 2; ++i) {
     CK(ctx->in_b[i].ensure(size_t(chunk) * pp * 8));
     CK(ctx->in_f[i].ensure(size_t(chunk) * pp * 8));
-    CK(ctx->out_T[i].ensure(size_t(chunk) * nb2 * 8));
-    CK(ctx->out_w[i].ensure(size_t(chunk) * d.nb * 8));
+    if (!dT_res) {
+      CK(ctx->out_T[i].ensure(size_t(chunk) * nb2 * 8));
+      CK(ctx->out_w[i].ensure(size_t(chunk) * d.nb * 8));
+    }
     CK(ctx->out_st[i].ensure(size_t(chunk) * 4));
     if (S) CK(ctx->out_S[i].ensure(size_t(chunk) * d.ni * d.nb * 8));
   }
@@ -792,7 +794,8 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
   // A D2H into pageable memory blocks the host thread until it completes, which would
   // serialise the pieces: pageable T/w land in pinned double buffers instead and are copied
   // out on the host while the next piece computes.
-  const bool stage = !pieces.empty() && !ctx->no_stage && !(host_pinned(T) && host_pinned(w));
+  const bool want_T = T != nullptr;
+  const bool stage = want_T && !pieces.empty() && !ctx->no_stage && !(host_pinned(T) && host_pinned(w));
   if (stage) {
     const int maxp = *std::max_element(pieces.begin(), pieces.end());
     for (int i = 0; i < 2; ++i) {
@@ -814,16 +817,17 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
     const int n = pieces[ci];
     const int k = ci & 1;
     const size_t off = size_t(c0 - e0);
-    double* T_dst = stage ? ctx->h_T[k].as<double>() : T + off * nb2;
-    double* w_dst = stage ? ctx->h_w[k].as<double>() : w + off * d.nb;
+    double* T_dst = stage ? ctx->h_T[k].as<double>() : want_T ? T + off * nb2 : nullptr;
+    double* w_dst = stage ? ctx->h_w[k].as<double>() : want_T ? w + off * d.nb : nullptr;
+    double* dT = dT_res ? dT_res + off * nb2 : ctx->out_T[k].as<double>();
+    double* dw = dw_res ? dw_res + off * d.nb : ctx->out_w[k].as<double>();
     CK(cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_in_free[k], 0));
     CK(cudaMemcpyAsync(ctx->in_b[k].ptr, b + off * pp, n * pp * 8, cudaMemcpyHostToDevice, ctx->s_h2d));
     CK(cudaMemcpyAsync(ctx->in_f[k].ptr, f + off * pp, n * pp * 8, cudaMemcpyHostToDevice, ctx->s_h2d));
     CK(cudaEventRecord(ctx->ev_in_ready[k], ctx->s_h2d));
     CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_in_ready[k], 0));
     CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_out_free[k], 0));
-    enqueue_condense_chunk(ctx, c0, n, ctx->in_b[k].as<double>(), ctx->in_f[k].as<double>(),
-                           ctx->out_T[k].as<double>(), ctx->out_w[k].as<double>(),
+    enqueue_condense_chunk(ctx, c0, n, ctx->in_b[k].as<double>(), ctx->in_f[k].as<double>(), dT, dw,
                            ctx->out_st[k].as<int>(), ctx->s_comp,
                            S != nullptr || ctx->desc.storage == HPS_STORAGE_STORE);
     if (S) {  // K3: S_solve from the factored workspace
@@ -839,8 +843,10 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
     CK(cudaEventRecord(ctx->ev_in_free[k], ctx->s_comp));
     CK(cudaEventRecord(ctx->ev_out_ready[k], ctx->s_comp));
     CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_out_ready[k], 0));
-    CK(cudaMemcpyAsync(T_dst, ctx->out_T[k].ptr, n * nb2 * 8, cudaMemcpyDeviceToHost, ctx->s_d2h));
-    CK(cudaMemcpyAsync(w_dst, ctx->out_w[k].ptr, n * size_t(d.nb) * 8, cudaMemcpyDeviceToHost, ctx->s_d2h));
+    if (want_T) {
+      CK(cudaMemcpyAsync(T_dst, dT, n * nb2 * 8, cudaMemcpyDeviceToHost, ctx->s_d2h));
+      CK(cudaMemcpyAsync(w_dst, dw, n * size_t(d.nb) * 8, cudaMemcpyDeviceToHost, ctx->s_d2h));
+    }
     CK(cudaMemcpyAsync(ctx->h_status.as<int32_t>() + off, ctx->out_st[k].ptr, n * 4, cudaMemcpyDeviceToHost,
                        ctx->s_d2h));
     if (S)
@@ -865,6 +871,56 @@ int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, 
   for (int i = 0; i < e1 - e0; ++i)
     if (status[i]) bad.push_back(e0 + i);
   if (!bad.empty()) return resonance_error(ctx, bad);
+  return HPS_OK;
+}
+
+int hps_gpu_condense(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, const double* f,
+                     double* T, double* w, double* S, int32_t* status) {
+  if (!ctx) return HPS_ERR_PARAM;
+  if (int rc = check_range(ctx, e0, e1)) return rc;
+  if (!b || !f || !T || !w || !status) return ctx->fail(HPS_ERR_PARAM, "ParameterError: null buffer");
+  return condense_pipeline(ctx, e0, e1, b, f, T, w, S, status, nullptr, nullptr);
+}
+
+// batched_condense + assemble_reduced in one call with T resident in HBM:
+// the host receives only the reduced system (CSR values + rhs) and, when asked, T/w.
+int hps_gpu_condense_assemble(hps_gpu_ctx* ctx, const double* b, const double* f, const double* g_bnd,
+                              double* values, double* rhs, double* T, double* w, int32_t* status) {
+  if (!ctx) return HPS_ERR_PARAM;
+  if (!b || !f || !g_bnd || !values || !rhs || !status || (!T) != (!w))
+    return ctx->fail(HPS_ERR_PARAM, "ParameterError: null buffer (T and w: both or neither)");
+  CK(cudaSetDevice(ctx->device));
+  const LeafDims& d = ctx->d;
+  const size_t nl = size_t(ctx->n_leaves), nb = size_t(d.nb);
+  const size_t ng = 2 * size_t(ctx->desc.nx * (d.p - 1) + 1) + 2 * size_t(ctx->desc.ny * (d.p - 1) + 1);
+  const int64_t na = ctx->mesh.n_active, nnz = ctx->mesh.nnz;
+  CK(ctx->k4_T.ensure(nl * nb * nb * 8));
+  CK(ctx->k4_w.ensure(nl * nb * 8));
+  CK(ctx->k4_g.ensure(ng * 8));
+  CK(ctx->k4_vals.ensure(size_t(std::max<int64_t>(1, nnz)) * 8));
+  CK(ctx->k4_rhs.ensure(size_t(std::max<int64_t>(1, na)) * 8));
+  CK(cudaMemcpyAsync(ctx->k4_g.ptr, g_bnd, ng * 8, cudaMemcpyHostToDevice, ctx->s_comp));
+  const int rc = condense_pipeline(ctx, 0, int(nl), b, f, T, w, nullptr, status, ctx->k4_T.as<double>(),
+                                   ctx->k4_w.as<double>());
+  if (rc != HPS_OK) return rc;   // resonance: the reduced system is not formed
+  if (na == 0) return HPS_OK;
+  cudaStream_t st = ctx->s_comp;
+  cudaEvent_t t0 = ctx->timing_event(3 * kTimingSlots), t1 = ctx->timing_event(3 * kTimingSlots + 1);
+  CK(cudaEventRecord(t0, st));
+  hpsg::launch_reduced_values(ctx->mesh_dev(), ctx->k4_T.as<double>(), ctx->k4_w.as<double>(), ctx->k4_g.as<double>(),
+                              ctx->k4_vals.as<double>(), ctx->k4_rhs.as<double>(), st, false);
+  CK(cudaEventRecord(t1, st));
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(values, ctx->k4_vals.ptr, size_t(nnz) * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(rhs, ctx->k4_rhs.ptr, size_t(na) * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  float ms = 0.0f;
+  cudaEventElapsedTime(&ms, t0, t1);
+  ctx->ms_scatter = ms;
+  ctx->tkernels += 1;
+  ctx->timing.ms_scatter = ms;
+  ctx->timing.ms_total += ms;
+  ctx->timing.kernels = ctx->tkernels;
   return HPS_OK;
 }
 

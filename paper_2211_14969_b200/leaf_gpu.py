@@ -66,7 +66,7 @@ EXPORTED = ["hps_gpu_create", "hps_gpu_destroy", "hps_gpu_last_error", "hps_gpu_
             "hps_gpu_multi_create", "hps_gpu_multi_destroy", "hps_gpu_multi_last_error", "hps_gpu_multi_shards",
             "hps_gpu_multi_ctx", "hps_gpu_multi_condense", "hps_gpu_multi_leaf_solve",
             "hps_gpu_multi_assemble_reduced", "hps_shard_range", "hps_reduced_cut_edges",
-            "hps_reduced_host_edges"]
+            "hps_reduced_host_edges", "hps_gpu_condense_assemble"]
 
 
 def lib():
@@ -99,7 +99,7 @@ def lib():
                      "hps_gpu_build_leaf_operator", "hps_gpu_condense_operator",
                      "hps_gpu_leaf_solve_operator", "hps_gpu_multi_shards", "hps_gpu_multi_condense",
                      "hps_gpu_multi_leaf_solve", "hps_gpu_multi_assemble_reduced", "hps_shard_range",
-                     "hps_reduced_cut_edges", "hps_reduced_host_edges"):
+                     "hps_reduced_cut_edges", "hps_reduced_host_edges", "hps_gpu_condense_assemble"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -344,6 +344,28 @@ class LeafStage:
         vals = np.empty(ci.size); rhs = np.empty(rp.size - 1)
         self._check(lib().hps_gpu_assemble_reduced(self._h, _ptr(T), _ptr(w), _ptr(g_bnd), _ptr(vals), _ptr(rhs)))
         return rp, ci, vals, rhs
+
+    def condense_assemble(self, b, f, g_bnd, want_T=False, out=None, raise_on_resonance=True):
+        """batched_condense + assemble_reduced of the whole mesh with T resident in HBM
+        (hps_gpu_condense_assemble): (row_ptr, col_idx, values, rhs, status[, T, w]).
+        `out`: optional caller-owned (values, rhs) arrays (pinned for full overlap)."""
+        pp = self.p * self.p
+        b = _rows(_f64(b, (-1, pp)), self.n_leaves, "b"); f = _rows(_f64(f, (-1, pp)), self.n_leaves, "f")
+        g_bnd = _f64(g_bnd, (-1,))
+        rp, ci = self.reduced_pattern()
+        if out is None:
+            vals = np.empty(ci.size); rhs = np.empty(rp.size - 1)
+        else:
+            vals = _out(out[0], (ci.size,), np.float64, "out values")
+            rhs = _out(out[1], (rp.size - 1,), np.float64, "out rhs")
+        T = np.empty((self.n_leaves, self.n_b, self.n_b)) if want_T else None
+        w = np.empty((self.n_leaves, self.n_b)) if want_T else None
+        st = np.zeros(self.n_leaves, np.int32)
+        rc = lib().hps_gpu_condense_assemble(self._h, _ptr(b), _ptr(f), _ptr(g_bnd), _ptr(vals), _ptr(rhs),
+                                             _ptr(T), _ptr(w), _ptr(st))
+        if rc != HPS_OK and (rc != HPS_ERR_RESONANCE or raise_on_resonance):
+            self._check(rc, st, 0)
+        return (rp, ci, vals, rhs, st, T, w) if want_T else (rp, ci, vals, rhs, st)
 
     def reduced_bsr_pattern(self):
         """BSR pattern of the reduced system (SPEC.md:331 ReducedSystem.blocks): block row =

@@ -475,3 +475,21 @@ def test_resonance_injection_blocked_kernels(p):
     r = O.batched_condense(p, 1.0 / nx, 4.0, b, f)
     ok = s == 0
     assert rel_fro(T[ok], r["T"][ok]).max() <= TOL_T
+
+
+@pytest.mark.parametrize("p,nx,ny,kappa", [(8, 6, 5, 12.0), (16, 5, 4, 40.0), (22, 6, 6, 100.0)])
+def test_condense_assemble_fused_equals_separate(p, nx, ny, kappa):
+    """hps_gpu_condense_assemble (T resident in HBM, only the reduced system comes back) is
+    bitwise condense + assemble_reduced; with want_T the T/w are the separate call's too."""
+    X, Y = P.leaf_coords(nx, ny, p)
+    b = P.crystal_field(0.3 + 0.4 * X, 0.3 + 0.4 * Y)
+    f = np.random.default_rng(3).uniform(-1, 1, X.shape)
+    gb = P.boundary_samples(nx, ny, p, lambda x, y: np.exp(x) * np.cos(y))
+    with G().LeafStage(p, nx, ny, kappa) as st:
+        T, w, s = st.condense(b, f)
+        rp, ci, va, rh = st.assemble_reduced(T, w, gb)
+        rp2, ci2, va2, rh2, s2 = st.condense_assemble(b, f, gb)
+        rp3, ci3, va3, rh3, s3, T3, w3 = st.condense_assemble(b, f, gb, want_T=True)
+    assert np.array_equal(va, va2) and np.array_equal(rh, rh2) and not s2.any()
+    assert np.array_equal(va, va3) and np.array_equal(rh, rh3)
+    assert np.array_equal(T, T3) and np.array_equal(w, w3)

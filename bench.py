@@ -139,7 +139,9 @@ def cpu_model():
 def b_star(cfg):
     """Resonant coefficient value of the workload: kappa^2 b* = lowest interior Dirichlet
     eigenvalue of a leaf of side a, ~2 pi^2 / a^2 (189,575 at C4 vs 2 pi^2 98^2 = 189,571)."""
-    return 2.0 * np.pi ** 2 / (cfg["a"] ** 2 * max(cfg["kappa"], 1e-300) ** 2)
+    if cfg["kappa"] == 0.0:
+        return float("inf")   # Laplace: no interior resonance
+    return 2.0 * np.pi ** 2 / (cfg["a"] ** 2 * cfg["kappa"] ** 2)
 
 
 def sample_order(cfg, b):

@@ -143,6 +143,19 @@ int hps_gpu_residual_device(hps_gpu_ctx* ctx, const double* d_b, const double* d
 int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, const double* f,
                        const double* v, double* u, int32_t* status);
 
+/* reconstruct_full_solution on the device: boundary vectors of every
+ * leaf from the reduced solution u_active (n_active, active_index order) and the Dirichlet
+ * samples g_bnd (hps_gpu_assemble_reduced layout), interiors by batched leaf_solve (b, f:
+ * all leaves' samples), placement into the full grid u_full (N values, g = gy*Nx + gx),
+ * element corners on Gamma from g and interior corners by the corner policy (SPEC.md:152:
+ * mean of the four adjacent edge interpolants).  status: per leaf (resonance).  The
+ * device variant also returns the local solutions (d_u_leaf, nullable; p*p per leaf). */
+int hps_gpu_reconstruct(hps_gpu_ctx* ctx, const double* u_active, const double* g_bnd, const double* b,
+                        const double* f, double* u_full, int32_t* status);
+int hps_gpu_reconstruct_device(hps_gpu_ctx* ctx, const double* d_u_active, const double* d_g_bnd,
+                               const double* d_b, const double* d_f, double* d_u_full, double* d_u_leaf,
+                               int32_t* d_status, void* stream);
+
 /* assemble_reduced — K4.  Pattern: CSR of the reduced system
  * over active nodes, int64 row_ptr (n_active+1), int32 col_idx
  * (nnz).  Call with row_ptr == NULL to get nnz only. */

@@ -280,100 +280,21 @@ std::vector<double> leaf_solve_on(hps_gpu_ctx* ctx, const MeshTopology& topo, co
   return u;
 }
 
-// reconstruct_full_solution: interface values from the reduced solution,
-// Dirichlet data on Gamma, interiors by batched leaf_solve (K5), interior corners by the
-// corner policy.
+// reconstruct_full_solution on the GPU (hps_gpu_reconstruct: K7 boundary
+// vectors, batched leaf_solve, placement, corner policy SPEC.md:152); the host only samples
+// b, f and g.
 std::vector<double> reconstruct_on(hps_gpu_ctx* ctx, const MeshTopology& topo, const ProblemSpec& spec,
                                    int workers, const std::vector<double>& u_active,
                                    const std::vector<double>& f_full) {
-  const int p = topo.params.p, nx = topo.params.nx, ny = topo.params.ny, nb = 4 * (p - 1);
-  const int n = nx * ny;
+  const int n = topo.params.nx * topo.params.ny;
   if (int64_t(u_active.size()) != topo.n_active) throw ParameterError("reduced solution size");
-  const int64_t Nx = int64_t(nx) * (p - 1) + 1, Ny = int64_t(ny) * (p - 1) + 1;
+  std::vector<double> b, f;
+  sample_leaves(topo, spec, 0, n, f_full, workers, b, f);
   const auto g = boundary_samples(topo, spec);
-  auto gval = [&](int64_t gx, int64_t gy) {
-    if (gy == 0) return g[gx];
-    if (gy == Ny - 1) return g[Nx + gx];
-    if (gx == 0) return g[2 * Nx + gy];
-    return g[2 * Nx + Ny + gy];
-  };
-  // boundary vectors per leaf (corners of interior edges do not enter: exact zero columns)
-  std::vector<double> v(size_t(n) * nb, 0.0);
-  for_elements(n, workers, [&](int e) {
-    const auto gid = topo.element_node_index(e);
-    for (int k = 0; k < nb; ++k) {
-      int iy, ix;
-      if (k < p) { iy = 0; ix = k; }
-      else if (k < 2 * p - 1) { iy = k - p + 1; ix = p - 1; }
-      else if (k < 3 * p - 2) { iy = p - 1; ix = k - 2 * p + 1; }
-      else { iy = k - 3 * p + 3; ix = 0; }
-      const int64_t gg = gid[iy * p + ix];
-      const int64_t act = topo.active_of_global(gg);
-      const int64_t gx = gg % Nx, gy = gg / Nx;
-      if (act >= 0) v[size_t(e) * nb + k] = u_active[act];
-      else if (gx == 0 || gy == 0 || gx == Nx - 1 || gy == Ny - 1) v[size_t(e) * nb + k] = gval(gx, gy);
-    }
-  });
-  const auto ul = leaf_solve_on(ctx, topo, spec, workers, 0, n, v, f_full);
-  std::vector<double> u(size_t(topo.N), 0.0);
-  // Each global node is written by exactly one element: its S/W sides and interior, plus the
-  // N (E) side on the top row (right column) of elements.
-  for_elements(n, workers, [&](int e) {
-    const int ex = e % nx, ey = e / nx;
-    const auto gid = topo.element_node_index(e);
-    for (int iy = 0; iy < p; ++iy)
-      for (int ix = 0; ix < p; ++ix)
-        if ((iy < p - 1 || ey == ny - 1) && (ix < p - 1 || ex == nx - 1))
-          u[gid[iy * p + ix]] = ul[size_t(e) * p * p + iy * p + ix];
-  });
-  // Interior corners: average of the degree-(p-3) interpolants of the
-  // adjacent interface edges (through their p-2 active nodes) evaluated at the corner.
-  const auto xh = cheb_nodes(p);
-  std::vector<double> wts(p - 2);
-  for (int j = 1; j <= p - 2; ++j) {
-    double prod = 1.0;
-    for (int k = 1; k <= p - 2; ++k)
-      if (k != j) prod *= (xh[j] - xh[k]);
-    wts[j - 1] = 1.0 / prod;
-  }
-  auto edge_extrap = [&](const double* vals, double t) {  // barycentric (2nd form) at t
-    double num = 0.0, den = 0.0;
-    for (int j = 0; j < p - 2; ++j) {
-      const double c = wts[j] / (t - xh[j + 1]);
-      num += c * vals[j];
-      den += c;
-    }
-    return num / den;
-  };
-  std::vector<double> vals(p - 2);
-  for (int cy = 1; cy < ny; ++cy)
-    for (int cx = 1; cx < nx; ++cx) {
-      const int64_t gx = int64_t(cx) * (p - 1), gy = int64_t(cy) * (p - 1);
-      double s = 0.0;
-      int cnt = 0;
-      for (int dir = 0; dir < 4; ++dir) {  // left, right (horizontal line), down, up (vertical)
-        for (int j = 1; j <= p - 2; ++j) {
-          int64_t x = gx, y = gy;
-          if (dir == 0) x = gx - (p - 1) + j;
-          if (dir == 1) x = gx + j;
-          if (dir == 2) y = gy - (p - 1) + j;
-          if (dir == 3) y = gy + j;
-          vals[j - 1] = u_active[topo.active_of_global(y * Nx + x)];
-        }
-        s += edge_extrap(vals.data(), (dir == 0 || dir == 2) ? 1.0 : -1.0);
-        ++cnt;
-      }
-      u[gy * Nx + gx] = s / cnt;
-    }
-  // Element corners on Gamma take the Dirichlet data.
-  for (int64_t gx = 0; gx < Nx; gx += p - 1) {
-    u[gx] = gval(gx, 0);
-    u[(Ny - 1) * Nx + gx] = gval(gx, Ny - 1);
-  }
-  for (int64_t gy = 0; gy < Ny; gy += p - 1) {
-    u[gy * Nx] = gval(0, gy);
-    u[gy * Nx + Nx - 1] = gval(Nx - 1, gy);
-  }
+  std::vector<double> u(size_t(topo.N));
+  std::vector<int32_t> st(n);
+  throw_rc(hps_gpu_reconstruct(ctx, u_active.data(), g.data(), b.data(), f.data(), u.data(), st.data()), ctx,
+           st.data(), 0, n);
   return u;
 }
 

@@ -251,6 +251,7 @@ struct hps_gpu_ctx {
   DevBuf field_off, field_cent;   // K0 crystal sampler: node offsets, centres
   DevBuf op_A, op_Dn, op_b, op_f, op_v, op_T, op_w, op_st, op_S, op_u;   // operator-path staging
   DevBuf k4_T, k4_w, k4_g, k4_vals, k4_rhs, k4_list;   // assemble_reduced (host buffers), persistent
+  DevBuf rc_ua, rc_g, rc_b, rc_f, rc_v, rc_ul, rc_u, rc_st, rc_tab;   // reconstruct_full_solution
   DevBuf res_flux, res_pl, res_pe, res_in;   // K6 residual scratch
   int store_e0 = -1, store_e1 = -1;
   HostBuf h_status;               // pinned staging of status[] (see HostBuf)
@@ -1023,6 +1024,58 @@ int hps_gpu_residual(hps_gpu_ctx* ctx, const double* b, const double* f, const d
   return hps_gpu_residual_device(ctx, d, d + n * pp, d + 2 * n * pp, out, ctx->s_comp);
 }
 
+// One chunk of batched leaf_solve on device buffers (elements [c0, c0 + n), n <= chunk):
+// recompute policy K1s [A_ii | f_i - A_ib v] -> K2 -> K5; store policy: rhs into the kept
+// condense workspace -> K2 trailing-only -> K5.
+static cudaError_t enqueue_leaf_solve_chunk(hps_gpu_ctx* ctx, int c0, int n, const double* d_b, const double* d_f,
+                                            const double* d_v, double* d_u, int* d_st, cudaStream_t st) {
+  const LeafDims& d = ctx->d;
+  const bool store = ctx->desc.storage == HPS_STORAGE_STORE;
+  const int slot = next_timing_slot(ctx);
+  ctx->tkernels += store ? 3 : 4;
+  cudaEventRecord(ctx->timing_event(3 * slot), st);
+  hpsg::LuArgs a;
+  a.ws = ctx->ws.as<double>();
+  a.linv = ctx->linv.as<double>();
+  a.perm = ctx->perm.as<short>();
+  a.norms = ctx->norms.as<double>();
+  a.T_out = nullptr;
+  a.w_out = nullptr;
+  a.status = d_st;
+  a.minratio = nullptr;
+  LeafDims dsolve;
+  if (store) {
+    // Kept condense factors: rhs into column tb0, trailing-only LU pass.
+    const size_t lo = size_t(c0 - ctx->store_e0);
+    dsolve = d;
+    dsolve.R = d.ni;
+    dsolve.ntb = 1;
+    a.ws += lo * d.leaf_stride;
+    a.linv += lo * d.nblk * 4096;
+    a.perm += lo * d.Rpad;
+    hpsg::launch_write_rhs(d, d.tb0, ctx->D2.as<double>(), d_f,
+                           d_v, a.ws, n, st);
+    cudaMemsetAsync(a.status, 0, n * 4, st);
+    a.factor = 0;
+  } else {
+    dsolve = ctx->ds;
+    const int* inj = ctx->has_inject ? ctx->inject_all.as<int>() + c0 : nullptr;
+    hpsg::launch_assemble_solve(dsolve, ctx->rowcode_s.as<int>(), ctx->colcode_s.as<int>(),
+                                ctx->Ds.as<double>(), ctx->D2.as<double>(), ctx->k2,
+                                d_b, d_f,
+                                d_v, a.ws, ctx->norms.as<double>(), inj, n, st);
+    a.factor = 1;
+  }
+  cudaEventRecord(ctx->timing_event(3 * slot + 1), st);
+  a.d = dsolve;
+  // (lock-step measured no faster for the leaf-solve factorisation: 10.63 vs 10.45 ms at C2)
+  hpsg::launch_lu_schur(a, n, st);
+  hpsg::launch_backsolve(dsolve, a.ws, a.perm, d_v, d_u,
+                         n, st);
+  cudaEventRecord(ctx->timing_event(3 * slot + 2), st);
+  return cudaGetLastError();
+}
+
 int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b, const double* f,
                        const double* v, double* u, int32_t* status) {
   if (!ctx) return HPS_ERR_PARAM;
@@ -1076,48 +1129,8 @@ int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b
     CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_in_ready[k], 0));
     CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_out_free[k], 0));
     cudaStream_t st = ctx->s_comp;
-    const int slot = next_timing_slot(ctx);
-    ctx->tkernels += store ? 3 : 4;
-    cudaEventRecord(ctx->timing_event(3 * slot), st);
-    hpsg::LuArgs a;
-    a.ws = ctx->ws.as<double>();
-    a.linv = ctx->linv.as<double>();
-    a.perm = ctx->perm.as<short>();
-    a.norms = ctx->norms.as<double>();
-    a.T_out = nullptr;
-    a.w_out = nullptr;
-    a.status = ctx->out_st[k].as<int>();
-    a.minratio = nullptr;
-    LeafDims dsolve;
-    if (store) {
-      // Kept condense factors: rhs into column tb0, trailing-only LU pass.
-      const size_t lo = size_t(c0 - ctx->store_e0);
-      dsolve = d;
-      dsolve.R = d.ni;
-      dsolve.ntb = 1;
-      a.ws += lo * d.leaf_stride;
-      a.linv += lo * d.nblk * 4096;
-      a.perm += lo * d.Rpad;
-      hpsg::launch_write_rhs(d, d.tb0, ctx->D2.as<double>(), ctx->in_f[k].as<double>(),
-                             ctx->in_v[k].as<double>(), a.ws, n, st);
-      CK(cudaMemsetAsync(a.status, 0, n * 4, st));
-      a.factor = 0;
-    } else {
-      dsolve = ctx->ds;
-      const int* inj = ctx->has_inject ? ctx->inject_all.as<int>() + c0 : nullptr;
-      hpsg::launch_assemble_solve(dsolve, ctx->rowcode_s.as<int>(), ctx->colcode_s.as<int>(),
-                                  ctx->Ds.as<double>(), ctx->D2.as<double>(), ctx->k2,
-                                  ctx->in_b[k].as<double>(), ctx->in_f[k].as<double>(),
-                                  ctx->in_v[k].as<double>(), a.ws, ctx->norms.as<double>(), inj, n, st);
-      a.factor = 1;
-    }
-    cudaEventRecord(ctx->timing_event(3 * slot + 1), st);
-    a.d = dsolve;
-    // (lock-step measured no faster for the leaf-solve factorisation: 10.63 vs 10.45 ms at C2)
-    hpsg::launch_lu_schur(a, n, st);
-    hpsg::launch_backsolve(dsolve, a.ws, a.perm, ctx->in_v[k].as<double>(), ctx->out_u[k].as<double>(),
-                           n, st);
-    cudaEventRecord(ctx->timing_event(3 * slot + 2), st);
+    CK(enqueue_leaf_solve_chunk(ctx, c0, n, ctx->in_b[k].as<double>(), ctx->in_f[k].as<double>(),
+                                ctx->in_v[k].as<double>(), ctx->out_u[k].as<double>(), ctx->out_st[k].as<int>(), st));
     CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev_in_free[k], st));
     CK(cudaEventRecord(ctx->ev_out_ready[k], st));
@@ -1278,6 +1291,97 @@ int hps_gpu_assemble_reduced(hps_gpu_ctx* ctx, const double* T, const double* w,
 int hps_gpu_assemble_reduced_bsr(hps_gpu_ctx* ctx, const double* T, const double* w,
                                  const double* g_bnd, double* bvalues, double* rhs) {
   return assemble_reduced_host(ctx, T, w, g_bnd, bvalues, rhs, true);
+}
+
+// ---------------------------------------------------------------------------
+// reconstruct_full_solution on the device (K7 + batched leaf_solve).
+// ---------------------------------------------------------------------------
+int hps_gpu_reconstruct_device(hps_gpu_ctx* ctx, const double* d_u_active, const double* d_g_bnd,
+                               const double* d_b, const double* d_f, double* d_u_full, double* d_u_leaf,
+                               int32_t* d_status, void* stream) {
+  if (!ctx) return HPS_ERR_PARAM;
+  if (!d_u_active || !d_g_bnd || !d_b || !d_f || !d_u_full || !d_status)
+    return ctx->fail(HPS_ERR_PARAM, "ParameterError: null device buffer");
+  const int n = ctx->n_leaves;
+  if (ctx->desc.storage == HPS_STORAGE_STORE && (ctx->store_e0 > 0 || ctx->store_e1 < n))
+    return ctx->fail(HPS_ERR_PARAM, "ParameterError: store policy: no kept factors for the whole mesh");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->s_comp;
+  const int p = ctx->d.p, nx = ctx->desc.nx, ny = ctx->desc.ny, nb = ctx->d.nb;
+  const size_t pp = size_t(p) * p;
+  // corner-policy tables: nodes and barycentric weights of the p-2 interior nodes
+  std::vector<double> tab(size_t(2 * p), 0.0);
+  {
+    const double den = 2.0 * double(p - 1);
+    for (int k = 0; k < p; ++k) tab[k] = std::sin(M_PI * double(2 * k - (p - 1)) / den);
+    for (int j = 1; j <= p - 2; ++j) {
+      double prod = 1.0;
+      for (int k = 1; k <= p - 2; ++k)
+        if (k != j) prod *= (tab[j] - tab[k]);
+      tab[p + j - 1] = 1.0 / prod;
+    }
+  }
+  CK(ctx->rc_tab.ensure(tab.size() * 8));
+  CK(ctx->rc_v.ensure(size_t(n) * nb * 8));
+  if (!d_u_leaf) {
+    CK(ctx->rc_ul.ensure(size_t(n) * pp * 8));
+    d_u_leaf = ctx->rc_ul.as<double>();
+  }
+  CK(cudaMemcpyAsync(ctx->rc_tab.ptr, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaStreamWaitEvent(st, ctx->ev_scratch, 0));
+  hpsg::launch_leaf_boundary(p, nx, ny, 0, n, d_u_active, d_g_bnd, ctx->rc_v.as<double>(), st);
+  for (int c0 = 0; c0 < n; c0 += ctx->chunk) {
+    const int m = std::min(ctx->chunk, n - c0);
+    CK(enqueue_leaf_solve_chunk(ctx, c0, m, d_b + size_t(c0) * pp, d_f + size_t(c0) * pp,
+                                ctx->rc_v.as<double>() + size_t(c0) * nb, d_u_leaf + size_t(c0) * pp, d_status + c0,
+                                st));
+  }
+  hpsg::launch_place(p, nx, ny, 0, n, d_u_leaf, d_u_full, st);
+  hpsg::launch_corners(p, nx, ny, ctx->rc_tab.as<double>(), ctx->rc_tab.as<double>() + p, d_u_active, d_g_bnd,
+                       d_u_full, st);
+  ctx->tkernels += 3;
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev_scratch, st));
+  CK(cudaStreamSynchronize(st));   // the host tables above are temporaries
+  return HPS_OK;
+}
+
+int hps_gpu_reconstruct(hps_gpu_ctx* ctx, const double* u_active, const double* g_bnd, const double* b,
+                        const double* f, double* u_full, int32_t* status) {
+  if (!ctx) return HPS_ERR_PARAM;
+  if (!u_active || !g_bnd || !b || !f || !u_full || !status)
+    return ctx->fail(HPS_ERR_PARAM, "ParameterError: null buffer");
+  CK(cudaSetDevice(ctx->device));
+  const int p = ctx->d.p, n = ctx->n_leaves;
+  const size_t pp = size_t(p) * p;
+  const int64_t na = ctx->mesh.n_active;
+  const int64_t Nx = int64_t(ctx->desc.nx) * (p - 1) + 1, Ny = int64_t(ctx->desc.ny) * (p - 1) + 1;
+  const size_t ng = size_t(2 * Nx + 2 * Ny), N = size_t(Nx * Ny);
+  CK(ctx->rc_ua.ensure(size_t(std::max<int64_t>(1, na)) * 8));
+  CK(ctx->rc_g.ensure(ng * 8));
+  CK(ctx->rc_b.ensure(size_t(n) * pp * 8));
+  CK(ctx->rc_f.ensure(size_t(n) * pp * 8));
+  CK(ctx->rc_u.ensure(N * 8));
+  CK(ctx->rc_st.ensure(size_t(n) * 4));
+  cudaStream_t st = ctx->s_comp;
+  reset_timing(ctx);
+  if (na > 0) CK(cudaMemcpyAsync(ctx->rc_ua.ptr, u_active, size_t(na) * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ctx->rc_g.ptr, g_bnd, ng * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ctx->rc_b.ptr, b, size_t(n) * pp * 8, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(ctx->rc_f.ptr, f, size_t(n) * pp * 8, cudaMemcpyHostToDevice, st));
+  const int rc = hps_gpu_reconstruct_device(ctx, ctx->rc_ua.as<double>(), ctx->rc_g.as<double>(),
+                                            ctx->rc_b.as<double>(), ctx->rc_f.as<double>(), ctx->rc_u.as<double>(),
+                                            nullptr, ctx->rc_st.as<int>(), st);
+  if (rc != HPS_OK) return rc;
+  CK(cudaMemcpyAsync(u_full, ctx->rc_u.ptr, N * 8, cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(status, ctx->rc_st.ptr, size_t(n) * 4, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  finish_timing(ctx);
+  std::vector<int> bad;
+  for (int i = 0; i < n; ++i)
+    if (status[i]) bad.push_back(i);
+  if (!bad.empty()) return resonance_error(ctx, bad);
+  return HPS_OK;
 }
 
 // ---------------------------------------------------------------------------

@@ -135,6 +135,13 @@ void launch_reduced_bsr_pattern(const MeshDev& m, int64_t* brow_ptr, int32_t* bc
 // Per-leaf scatter map for leaves [e0, e0+n): slot (n x nb x nb) into the CSR values, row (n x nb).
 void launch_scatter_indices(const MeshDev& m, int e0, int n, int64_t* slot, int64_t* row, cudaStream_t st);
 
+// K7 (k7_reconstruct.cu): reconstruct_full_solution pieces.
+void launch_leaf_boundary(int p, int nx, int ny, int e0, int n, const double* ua, const double* g, double* v,
+                          cudaStream_t st);
+void launch_place(int p, int nx, int ny, int e0, int n, const double* ul, double* u, cudaStream_t st);
+void launch_corners(int p, int nx, int ny, const double* xh, const double* wts, const double* ua, const double* g,
+                    double* u, cudaStream_t st);
+
 // K6: matrix-free residual of the global collocation system (k6_residual.cu): per-leaf
 // [sum r_int^2, sum f_int^2] into part_leaf (2 per leaf), per-edge sum r_flux^2 into
 // part_edge, outward fluxes (nb per leaf) into the flux scratch.

@@ -66,7 +66,8 @@ EXPORTED = ["hps_gpu_create", "hps_gpu_destroy", "hps_gpu_last_error", "hps_gpu_
             "hps_gpu_multi_create", "hps_gpu_multi_destroy", "hps_gpu_multi_last_error", "hps_gpu_multi_shards",
             "hps_gpu_multi_ctx", "hps_gpu_multi_condense", "hps_gpu_multi_leaf_solve",
             "hps_gpu_multi_assemble_reduced", "hps_shard_range", "hps_reduced_cut_edges",
-            "hps_reduced_host_edges", "hps_gpu_condense_assemble"]
+            "hps_reduced_host_edges", "hps_gpu_condense_assemble", "hps_gpu_reconstruct",
+            "hps_gpu_reconstruct_device"]
 
 
 def lib():
@@ -99,7 +100,8 @@ def lib():
                      "hps_gpu_build_leaf_operator", "hps_gpu_condense_operator",
                      "hps_gpu_leaf_solve_operator", "hps_gpu_multi_shards", "hps_gpu_multi_condense",
                      "hps_gpu_multi_leaf_solve", "hps_gpu_multi_assemble_reduced", "hps_shard_range",
-                     "hps_reduced_cut_edges", "hps_reduced_host_edges", "hps_gpu_condense_assemble"):
+                     "hps_reduced_cut_edges", "hps_reduced_host_edges", "hps_gpu_condense_assemble",
+                     "hps_gpu_reconstruct", "hps_gpu_reconstruct_device"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -310,6 +312,20 @@ class LeafStage:
         u = np.empty((n, pp)); st = np.zeros(n, np.int32)
         rc = lib().hps_gpu_leaf_solve_operator(self._h, e0, e0 + n, _ptr(A), _ptr(f), _ptr(v), _ptr(u), _ptr(st))
         self._check(rc, st, e0)
+        return u
+
+    def reconstruct(self, u_active, g_bnd, b, f):
+        """reconstruct_full_solution on the GPU: the full-grid solution
+        (N values, g = gy*Nx + gx) from the reduced solution and g_bnd; b, f all leaves."""
+        pp = self.p * self.p
+        b = _rows(_f64(b, (-1, pp)), self.n_leaves, "b"); f = _rows(_f64(f, (-1, pp)), self.n_leaves, "f")
+        ua = _f64(u_active, (-1,)); g_bnd = _f64(g_bnd, (-1,))
+        info = self.info()
+        if ua.size != info["n_active"]:
+            raise ParameterError(f"u_active: {ua.size} values, {info['n_active']} expected")
+        u = np.empty(info["N"]); st = np.zeros(self.n_leaves, np.int32)
+        self._check(lib().hps_gpu_reconstruct(self._h, _ptr(ua), _ptr(g_bnd), _ptr(b), _ptr(f), _ptr(u), _ptr(st)),
+                    st, 0)
         return u
 
     # -- assemble_reduced ---------------------------------------------------------------------

@@ -493,3 +493,53 @@ def test_condense_assemble_fused_equals_separate(p, nx, ny, kappa):
     assert np.array_equal(va, va2) and np.array_equal(rh, rh2) and not s2.any()
     assert np.array_equal(va, va3) and np.array_equal(rh, rh3)
     assert np.array_equal(T, T3) and np.array_equal(w, w3)
+
+
+@pytest.mark.parametrize("p,nx,ny,kappa", [(8, 4, 3, 9.0), (14, 5, 4, 30.0), (22, 3, 3, 60.0)])
+def test_reconstruct_on_device(p, nx, ny, kappa):
+    """hps_gpu_reconstruct (K7 + batched leaf_solve): every non-corner node is
+    bitwise the GPU leaf_solve of the host-built boundary vectors, element corners on Gamma are
+    g, and interior corners follow the corner policy -- restated here in the same
+    IEEE operation order, so they agree bit for bit."""
+    X, Y = P.leaf_coords(nx, ny, p)
+    b = P.crystal_field(0.3 + 0.4 * X, 0.3 + 0.4 * Y)
+    f = np.random.default_rng(9).uniform(-1, 1, X.shape)
+    gb = P.boundary_samples(nx, ny, p, lambda x, y: np.cos(2 * x) * (1 + y))
+    _, _, na = O.mesh_info(nx, ny, p)
+    ua = np.random.default_rng(4).uniform(-1, 1, na)
+    with G().LeafStage(p, nx, ny, kappa) as st:
+        u = st.reconstruct(ua, gb, b, f)
+        v = H.leaf_boundary_values(nx, ny, p, ua, gb)
+        ul = st.leaf_solve(b, f, v)
+    ref = H.scatter_full(nx, ny, p, ul)
+    cls = H.classify(nx, ny, p)
+    Nx = nx * (p - 1) + 1
+    gx = np.arange(u.size) % Nx; gy = np.arange(u.size) // Nx
+    corner = (gx % (p - 1) == 0) & (gy % (p - 1) == 0)
+    assert np.array_equal(u[~corner], ref[~corner])
+    # corner policy restated (hps_api.cpp / k7_corner_kernel order)
+    xh = P.cheb_nodes(p)
+    wts = [1.0 / np.prod([xh[j] - xh[k] for k in range(1, p - 1) if k != j]) for j in range(1, p - 1)]
+    act = lambda x, y: O.active_of_global(nx, ny, p, np.array([y * Nx + x]))[0]
+    for cy in range(ny + 1):
+        for cx in range(nx + 1):
+            X0, Y0 = cx * (p - 1), cy * (p - 1)
+            g = Y0 * Nx + X0
+            if cls[g] == 2:
+                assert u[g] == ref[g]
+                continue
+            s = 0.0
+            for d in range(4):
+                t = 1.0 if d in (0, 2) else -1.0
+                num = den = 0.0
+                for j in range(1, p - 1):
+                    x, y = X0, Y0
+                    if d == 0: x = X0 - (p - 1) + j
+                    if d == 1: x = X0 + j
+                    if d == 2: y = Y0 - (p - 1) + j
+                    if d == 3: y = Y0 + j
+                    c = wts[j - 1] / (t - xh[j])
+                    num = num + c * ua[act(x, y)]
+                    den = den + c
+                s = s + num / den
+            assert u[g] == s / 4.0, (cx, cy)

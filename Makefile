@@ -21,7 +21,9 @@ G128_NSTAGE ?= 2
 G128_KC     ?= 16
 OBJS      := $(patsubst $(SRC)/%,$(OBJDIR)/%.o,$(CU) $(CPP)) $(K2OBJS)
 
-all: $(LIB) oracle
+SLIB      := paper_2211_14969_b200/_lib/libhps_slablu_b200.so
+
+all: $(LIB) $(SLIB) oracle
 
 $(OBJDIR)/%.cu.o: $(SRC)/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
@@ -45,11 +47,20 @@ $(LIB): $(OBJS)
 	@mkdir -p $(dir $@)
 	$(NVCC) $(ARCH) -shared -cudart static -o $@ $(OBJS)
 
+# GPU SlabLU: its own library, cuSOLVER/cuBLAS for the dense blocks.
+$(OBJDIR)/slablu.o: $(SRC)/slablu.cu include/hps_slablu.h
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ > $(OBJDIR)/slablu.ptxas.log 2>&1 || (cat $(OBJDIR)/slablu.ptxas.log; exit 1)
+
+$(SLIB): $(OBJDIR)/slablu.o
+	@mkdir -p $(dir $@)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@ $< -lcusolver -lcublas
+
 oracle:
 	$(MAKE) -s -C oracle
 
 clean:
-	rm -rf build $(LIB)
+	rm -rf build $(LIB) $(SLIB)
 	$(MAKE) -s -C oracle clean
 
 .PHONY: all oracle clean cxx_test

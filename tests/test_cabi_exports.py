@@ -8,23 +8,28 @@ from paper_2211_14969_b200 import leaf_gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def declared_functions():
-    names = set()
-    for fn in os.listdir(os.path.join(ROOT, "include")):
-        if fn.endswith(".h"):
-            src = open(os.path.join(ROOT, "include", fn)).read()
-            src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-            names |= set(re.findall(r"\b(hps_\w+)\s*\(", src))
-    return names
+LIBS = {"hps_leaf_gpu.h": lambda: leaf_gpu.LIB_PATH,
+        "hps_slablu.h": lambda: os.path.join(ROOT, "paper_2211_14969_b200", "_lib", "libhps_slablu_b200.so")}
+
+
+def declared_functions(header):
+    src = open(os.path.join(ROOT, "include", header)).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return set(re.findall(r"\b(hps_\w+)\s*\(", src))
+
+
+def test_every_header_has_a_library():
+    assert sorted(f for f in os.listdir(os.path.join(ROOT, "include")) if f.endswith(".h")) == sorted(LIBS)
 
 
 def test_library_exports_every_declared_symbol():
-    lib = ctypes.CDLL(leaf_gpu.LIB_PATH)
-    decl = declared_functions()
-    assert len(decl) >= 15
-    missing = [n for n in sorted(decl) if not hasattr(lib, n)]
-    assert not missing, missing
-    assert set(leaf_gpu.EXPORTED) <= decl
+    for header, path in LIBS.items():
+        lib = ctypes.CDLL(path())
+        decl = declared_functions(header)
+        assert len(decl) >= 5, header
+        missing = [n for n in sorted(decl) if not hasattr(lib, n)]
+        assert not missing, (header, missing)
+    assert set(leaf_gpu.EXPORTED) <= declared_functions("hps_leaf_gpu.h")
 
 
 def test_version_string_without_gpu():

@@ -19,6 +19,7 @@ import hps_harness as H
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C2")
 ap.add_argument("--out", default="")
+ap.add_argument("--slab-width", type=int, default=0)
 a = ap.parse_args()
 cfg = P.config(a.config)
 p, nx, ny, kappa = cfg["p"], cfg["nx"], cfg["ny"], cfg["kappa"]
@@ -40,6 +41,15 @@ with G.LeafStage(p, nx, ny, kappa) as st:
     assert np.array_equal(pv, vals) and np.array_equal(pr, rhs)
     A = sp.csr_matrix((vals, ci, rp), shape=(rp.size - 1, rp.size - 1))
     t0 = time.perf_counter(); ua = spla.spsolve(A.tocsc(), rhs); t["host_superlu_s"] = time.perf_counter() - t0
+    # GPU SlabLU on the BSR view of the same system
+    from paper_2211_14969_b200 import slab_gpu as SG
+    brp, bci, bva, brh = st.assemble_reduced_bsr(T, w, gb)
+    t0 = time.perf_counter()
+    with SG.SlabLU(p, nx, ny, brp, bci, bva, slab_width=a.slab_width) as lu:
+        t["slablu_factor_s"] = time.perf_counter() - t0
+        t0 = time.perf_counter(); ua_s = lu.solve(rhs); t["slablu_solve_s"] = time.perf_counter() - t0
+        t["slablu_info"] = lu.get_info()
+    t["slablu_vs_superlu_relerr"] = float(np.max(np.abs(ua_s - ua)) / np.max(np.abs(ua)))
     v = H.leaf_boundary_values(nx, ny, p, ua, gb)
     t0 = time.perf_counter(); ul = st.leaf_solve(b, f, v); t["leaf_solve_s"] = time.perf_counter() - t0
     t0 = time.perf_counter(); res = st.residual(b, f, ul); t["residual_s"] = time.perf_counter() - t0
@@ -49,7 +59,7 @@ g2 = float(np.sum(P.gaussian_pulse(gx, gy)[cls == 2] ** 2))
 relerr = math.sqrt((res["r_int2"] + res["r_flux2"]) / (res["f_int2"] + g2))
 N = (nx * (p - 1) + 1) * (ny * (p - 1) + 1)
 out = dict(config=a.config, p=p, nx=nx, ny=ny, kappa=kappa, dof=N, n_active=int(rp.size - 1), nnz=int(ci.size),
-           resonant=int(s.sum()), relerr_res=relerr, **{k: round(v_, 4) for k, v_ in t.items()})
+           resonant=int(s.sum()), relerr_res=relerr, **{k: (round(v_, 4) if isinstance(v_, float) and k.endswith(("_s", "_ms")) else v_) for k, v_ in t.items()})
 print(json.dumps(out))
 if a.out:
     json.dump(out, open(a.out, "w"), indent=1)

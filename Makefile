@@ -8,7 +8,7 @@ NVFLAGS   := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-ffp-contract=off
 SRC       := paper_2211_14969_b200/csrc
 OBJDIR    := build/obj
 LIB       := paper_2211_14969_b200/_lib/libhps_leaf_b200.so
-CU        := $(SRC)/k0_fields.cu $(SRC)/k1_assemble.cu $(SRC)/k1_operator.cu $(SRC)/k2s_small.cu $(SRC)/k4_scatter.cu $(SRC)/k5_leaf_solve.cu $(SRC)/k6_residual.cu $(SRC)/k7_reconstruct.cu
+CU        := $(SRC)/k0_fields.cu $(SRC)/k1_assemble.cu $(SRC)/k1_operator.cu $(SRC)/k2s_small.cu $(SRC)/k4_scatter.cu $(SRC)/k5_leaf_solve.cu $(SRC)/k6_residual.cu $(SRC)/k7_reconstruct.cu $(SRC)/k9_fp64_peak.cu
 CPP       := $(SRC)/hps_host.cpp $(SRC)/hps_api.cpp
 HDRS      := $(wildcard $(SRC)/*.h $(SRC)/*.cuh include/*.h include/hps/*.hpp)
 # K2/K3 are built twice: 8-warp CTAs (g256) and 4-warp CTAs for small leaves (g128).

@@ -33,8 +33,9 @@ sys.path.insert(0, ROOT)
 from paper_2211_14969_b200 import problems as P  # noqa: E402
 
 METRIC = "leaf-condensation leaves/s & DOF/s at p=22/42 (1/2/4/8 B200), FP64 TFLOP/s vs peak"
-FP64_PEAK_TFLOPS = 37.1   # measured DMMA m8n8k4 loop on this pool's B200 (profiles/r01_fp64_peak.log)
-FP64_PEAK_NOTE = "measured DMMA loop, profiles/r01_fp64_peak.log (MEASURED_PEAKS.json has no FP64 entry)"
+FP64_PEAK_TFLOPS = 37.1   # fallback: DMMA m8n8k4 loop on this pool's B200 (profiles/r01_fp64_peak.log)
+FP64_PEAK_NOTE = ("measured in this run on this GPU: register-only DMMA m8n8k4 loop, hps_gpu_fp64_peak_tflops "
+                  "(MEASURED_PEAKS.json and B200_PROFILING.md have no FP64 figure)")
 
 
 def parse():
@@ -314,6 +315,11 @@ def main():
     b, f = leaf_inputs(cfg, e0, e1)
     stage = G.LeafStage(p, cfg["nx"], cfg["ny"], cfg["kappa"], a=cfg["a"], device=local)
     info = stage.info()
+    try:
+        peak = G.fp64_peak_tflops(local)
+        peak_note = FP64_PEAK_NOTE
+    except Exception:
+        peak, peak_note = FP64_PEAK_TFLOPS, "fallback: profiles/r01_fp64_peak.log (live probe failed)"
 
     # ---- device-resident arm (value) ----
     dev = torch.device("cuda", local)
@@ -404,9 +410,9 @@ def main():
                       "ms_per_step_device": dev_ms / k_ls, "ms_assemble": k1_ms / k_ls,
                       "ms_lu_backsolve": k2k5_ms / k_ls,
                       "roofline": {"bound": "tensor", "flops_per_leaf": f_ls,
-                                   "achieved": n * f_ls / (k2k5_ms / k_ls / 1e3) / 1e12, "peak": FP64_PEAK_TFLOPS,
+                                   "achieved": n * f_ls / (k2k5_ms / k_ls / 1e3) / 1e12, "peak": peak,
                                    "unit": "TFLOP/s",
-                                   "frac": n * f_ls / (k2k5_ms / k_ls / 1e3) / 1e12 / FP64_PEAK_TFLOPS,
+                                   "frac": n * f_ls / (k2k5_ms / k_ls / 1e3) / 1e12 / peak,
                                    "note": "F_leafsolve = 2/3 n_i^3 + 2 n_i^2 + 2 n_i n_b (SURVEY 8d) over the "
                                            "K2+K5 device time"},
                       "h2d_bytes_per_step": int(n * (2 * p * p + nb) * 8), "d2h_bytes_per_step": int(n * p * p * 8)}
@@ -446,6 +452,7 @@ def main():
                      "dof_per_s": v2 * c2["N"] / c2["n_leaves"],
                      "tflops": v2 * P.flops_condense(22) / 1e12,
                      "k2_tflops": (s1 - s0) * P.flops_condense(22) / (t2["ms_lu_schur"] / args.steps / 1e3) / 1e12,
+                     "k2_frac": (s1 - s0) * P.flops_condense(22) / (t2["ms_lu_schur"] / args.steps / 1e3) / 1e12 / peak,
                      "ms_per_step": ms2 / args.steps}
         st2.close()
 
@@ -475,10 +482,10 @@ def main():
             "config": workload_config(cfg, world),
             "dof_per_s": value * cfg["N"] / cfg["n_leaves"],
             "tflops": value * f_leaf / 1e12,
-            "fp64_peak_frac": value * f_leaf / 1e12 / (FP64_PEAK_TFLOPS * world),
+            "fp64_peak_frac": value * f_leaf / 1e12 / (peak * world),
             "roofline": {"bound": "tensor", "kernel": k2_kernel_name(p), "achieved": achieved,
-                         "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
-                         "traffic": traffic, "peak_source": FP64_PEAK_NOTE,
+                         "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                         "traffic": traffic, "peak_source": peak_note,
                          "flops_per_leaf": f_leaf, "k2_ms_per_step_rank0": k2_ms,
                          "traffic_unit": "DRAM bytes per K2 launch (ncu, scaled to the launch's leaves)",
                          "k1_ms_per_step_rank0": tim["ms_assemble"] / args.steps},

@@ -257,6 +257,10 @@ int hps_reduced_host_edges(int32_t p, int32_t nx, int32_t ny, const int32_t* edg
 void* hps_host_alloc(size_t bytes);
 void hps_host_free(void* ptr);
 
+/* FP64 tensor (DMMA) peak of `device` in TF/s, measured now with a register-only
+ * mma.sync.m8n8k4.f64 loop (~0.1 s): the roofline denominator of K2/K3. */
+double hps_gpu_fp64_peak_tflops(int device);
+
 /* Library identity (for load checks). */
 const char* hps_gpu_version(void);
 

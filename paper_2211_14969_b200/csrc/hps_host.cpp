@@ -498,7 +498,12 @@ void enqueue_condense_chunk(hps_gpu_ctx* ctx, int e, int n, const double* d_b, c
 // ============================================================================
 extern "C" {
 
-const char* hps_gpu_version(void) { return "hps_leaf_b200 0.1 (sm_100a, DMMA f64)"; }
+const char* hps_gpu_version(void) { return "hps_leaf_b200 0.2 (sm_100a, DMMA f64)"; }
+
+double hps_gpu_fp64_peak_tflops(int device) {
+  if (cudaSetDevice(device) != cudaSuccess) return 0.0;
+  return hpsg::measure_dmma_peak_tflops(device);
+}
 
 void* hps_host_alloc(size_t bytes) {
   void* p = nullptr;

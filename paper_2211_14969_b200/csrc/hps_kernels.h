@@ -142,6 +142,9 @@ void launch_place(int p, int nx, int ny, int e0, int n, const double* ul, double
 void launch_corners(int p, int nx, int ny, const double* xh, const double* wts, const double* ua, const double* g,
                     double* u, cudaStream_t st);
 
+// FP64 tensor peak probe (k9_fp64_peak.cu): TF/s of a register-only DMMA loop on `device`.
+double measure_dmma_peak_tflops(int device);
+
 // K6: matrix-free residual of the global collocation system (k6_residual.cu): per-leaf
 // [sum r_int^2, sum f_int^2] into part_leaf (2 per leaf), per-edge sum r_flux^2 into
 // part_edge, outward fluxes (nb per leaf) into the flux scratch.

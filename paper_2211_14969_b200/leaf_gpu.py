@@ -67,7 +67,7 @@ EXPORTED = ["hps_gpu_create", "hps_gpu_destroy", "hps_gpu_last_error", "hps_gpu_
             "hps_gpu_multi_ctx", "hps_gpu_multi_condense", "hps_gpu_multi_leaf_solve",
             "hps_gpu_multi_assemble_reduced", "hps_shard_range", "hps_reduced_cut_edges",
             "hps_reduced_host_edges", "hps_gpu_condense_assemble", "hps_gpu_reconstruct",
-            "hps_gpu_reconstruct_device"]
+            "hps_gpu_reconstruct_device", "hps_gpu_fp64_peak_tflops"]
 
 
 def lib():
@@ -80,6 +80,8 @@ def lib():
         L.hps_gpu_last_error.restype = C.c_char_p
         L.hps_gpu_last_error.argtypes = [C.c_void_p]
         L.hps_gpu_version.restype = C.c_char_p
+        L.hps_gpu_fp64_peak_tflops.restype = C.c_double
+        L.hps_gpu_fp64_peak_tflops.argtypes = [C.c_int]
         L.hps_gpu_create.argtypes = [C.c_int, C.POINTER(_Desc), C.POINTER(C.c_void_p)]
         L.hps_gpu_destroy.argtypes = [C.c_void_p]
         L.hps_host_alloc.restype = C.c_void_p
@@ -401,6 +403,14 @@ class LeafStage:
         vals = np.empty((ci.size, q, q)); rhs = np.empty((rp.size - 1) * q)
         self._check(lib().hps_gpu_assemble_reduced_bsr(self._h, _ptr(T), _ptr(w), _ptr(g_bnd), _ptr(vals), _ptr(rhs)))
         return rp, ci, vals, rhs
+
+
+def fp64_peak_tflops(device=0):
+    """FP64 tensor (DMMA) peak of the GPU measured now (hps_gpu_fp64_peak_tflops)."""
+    v = lib().hps_gpu_fp64_peak_tflops(device)
+    if not v > 0:
+        raise CudaError("FP64 peak probe failed")
+    return v
 
 
 def shard_range(n, k, i):

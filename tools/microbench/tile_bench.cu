@@ -4,6 +4,7 @@
 #include "../../paper_2211_14969_b200/csrc/k2_lu_schur.cu"
 
 using namespace hpsg;
+using namespace hpsg::g256;
 
 template <class TL, bool HOT = false>
 __global__ void __launch_bounds__(NT, 2) tile_bench_kernel(double* ws, int ld, int K, int reps) {
@@ -30,7 +31,8 @@ __global__ void __launch_bounds__(NT, 2) tile_bench_kernel(double* ws, int ld, i
     auto crow = [=](int i) -> double* { return const_cast<double*>(M) + (size_t)perm[rt + i] * ld + 1536; };
     Acc acc;
     auto init = [&](Acc& x) { acc_load<TL>(x, crow, TM_); };
-    tile_mma<TL>(acc, init, arow, brow, K, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
+    tile_mma<TL>(Grp{(int)threadIdx.x, 0}, acc, init, arow, brow, K, -1.0, sm->pipe, sm->full, sm->empty,
+                 &sm->gchunk);
     acc_store<TL>(acc, crow, TM_, TL::WN * 32);
   }
 }
@@ -68,12 +70,12 @@ __global__ void __launch_bounds__(NT, 2) compute_only_kernel(double* out, int nc
   for (int c = 0; c < nch; ++c) {
     if (BARRIER) __syncthreads();
     const double* As = sm->pipe + (c % NSTAGE) * TL::STAGE;
-    const double* Bs = As + (TL::WM * 32) * LDA_S;
+    const double* Bs = As + (TL::WM * 32) * TL::LDA;
 #pragma unroll
     for (int kk = 0; kk < KC / 4; ++kk) {
       double a[4], b[4];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) a[mi] = -As[(32 * wm + 8 * mi + g) * LDA_S + 4 * kk + t];
+      for (int mi = 0; mi < 4; ++mi) a[mi] = -As[(32 * wm + 8 * mi + g) * TL::LDA + 4 * kk + t];
 #pragma unroll
       for (int ni = 0; ni < 4; ++ni) b[ni] = Bs[(4 * kk + t) * TL::LDB + 32 * wn + 8 * ni + g];
 #pragma unroll
@@ -126,6 +128,7 @@ int main() {
     run<TileL>("128x64", ctas, 1024, 40, ws, ld);
     run<TileU>("64x128", ctas, 1024, 40, ws, ld);
     run<TileL>("128x64", ctas, 256, 160, ws, ld);
+    run<TileL>("128x64", ctas, 64, 400, ws, ld);
     run<TileL, true>("128x64", ctas, 1024, 40, ws, ld);
   }
   return 0;

@@ -12,7 +12,6 @@ import numpy as np
 import torch
 from paper_2211_14969_b200 import leaf_gpu as G, problems as P
 
-PEAK_TF = 37.1   # measured DMMA f64 loop (profiles/r01_fp64_peak.log)
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--ps", default="8,12,16,22,27,32,37,42")
@@ -20,7 +19,10 @@ ap.add_argument("--gpus-share", type=int, default=8)
 ap.add_argument("--kappa", type=float, default=500.0)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--out", default="")
+ap.add_argument("--parity-leaves", type=int, default=64,
+                help="leaves of the slice checked against the CPU oracle at each p (most crystal-varying first)")
 a = ap.parse_args()
+PEAK_TF = G.fp64_peak_tflops(0)   # measured now on this GPU (DMMA m8n8k4 register loop)
 
 rows = []
 for p in [int(x) for x in a.ps.split(",")]:
@@ -47,6 +49,24 @@ for p in [int(x) for x in a.ps.split(",")]:
             best = tm
     torch.cuda.synchronize()
     bad = int((s != 0).sum().item())
+    parity = None
+    if a.parity_leaves > 0:
+        # the crystal region (b varies; rank 0's slice is b = 1): a band of elements through the
+        # middle of the mesh, condensed on the GPU and by the CPU oracle
+        from oracle import pyoracle as O
+        mid = (nx // 2) * nx
+        ids = np.arange(mid, min(nx * nx, mid + nx))
+        Xc, Yc = P.leaf_coords(nx, nx, p, elements=ids)
+        bc = P.crystal_field(Xc, Yc)
+        sel = np.argsort(-(bc.max(axis=1) - bc.min(axis=1)), kind="stable")[:a.parity_leaves]
+        bsel = np.ascontiguousarray(bc[sel]); fsel = np.zeros_like(bsel)
+        Tg, _, _ = st.condense(bsel, fsel, raise_on_resonance=False)
+        ref = O.batched_condense(p, 1.0 / nx, a.kappa, bsel, fsel, workers=0, raise_on_resonance=False)
+        ok = ref["status"] == 0
+        num = np.linalg.norm((Tg - ref["T"]).reshape(sel.size, -1), axis=1)
+        den = np.linalg.norm(ref["T"].reshape(sel.size, -1), axis=1)
+        parity = dict(leaves=int(ok.sum()), max_relfro_T=float((num / den)[ok].max()), bar=1e-10,
+                      b_range_min=float((bc.max(axis=1) - bc.min(axis=1))[sel].min()))
     info = st.info()
     st.close()
     ms = best["ms_total"]
@@ -56,7 +76,7 @@ for p in [int(x) for x in a.ps.split(",")]:
                ms_k1=best["ms_assemble"], ms_k2=best["ms_lu_schur"], chunks=best["chunks"],
                leaves_per_s=n / (ms * 1e-3), dof_per_s_8gpu_equiv=N / (ms * 1e-3),
                tflops=tf, tflops_k2=tf_k2, frac_peak=tf / PEAK_TF, frac_peak_k2=tf_k2 / PEAK_TF,
-               resident_ctas=info["resident_ctas"], resonant=bad)
+               resident_ctas=info["resident_ctas"], resonant=bad, parity=parity)
     rows.append(row)
     print(json.dumps(row), flush=True)
     del b, f, T, w, s

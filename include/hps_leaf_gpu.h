@@ -215,6 +215,14 @@ int hps_gpu_condense_operator(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const do
 int hps_gpu_leaf_solve_operator(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* A_loc, const double* f,
                                 const double* v, double* u, int32_t* status);
 
+/* Kernel-path selection (results are the same to 1e-12; the default picks the faster one):
+ *   HPS_OPT_SMALL_KERNEL  register-resident K2s for 4 <= p <= 12 (default on)
+ *   HPS_OPT_LOCKSTEP      lock-step 4-leaf K2 CTAs for R <= 640, p <= 24 (default on)
+ * value: -1 default, 0 off, 1 on.  For tests and A/B measurements. */
+#define HPS_OPT_SMALL_KERNEL 1
+#define HPS_OPT_LOCKSTEP 2
+int hps_gpu_set_option(hps_gpu_ctx* ctx, int32_t option, int32_t value);
+
 /* Test hook: zero interior row 0 of A_ii for these element
  * ids, which forces a zero pivot.  n = 0 clears. */
 int hps_gpu_set_fault_injection(hps_gpu_ctx* ctx, const int32_t* elements, int32_t n);

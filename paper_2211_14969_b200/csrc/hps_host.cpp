@@ -680,6 +680,25 @@ int hps_gpu_reset_timing(hps_gpu_ctx* ctx) {
   return HPS_OK;
 }
 
+int hps_gpu_set_option(hps_gpu_ctx* ctx, int32_t option, int32_t value) {
+  if (!ctx) return HPS_ERR_PARAM;
+  if (value < -1 || value > 1) return ctx->fail(HPS_ERR_PARAM, "ParameterError: option value must be -1, 0 or 1");
+  switch (option) {
+    case HPS_OPT_SMALL_KERNEL:
+      if (value == 1 && !hpsg::small_condense_supported(ctx->d.p))
+        return ctx->fail(HPS_ERR_PARAM, "ParameterError: the register-resident kernel needs 4 <= p <= 12");
+      ctx->small_env = value;
+      return HPS_OK;
+    case HPS_OPT_LOCKSTEP:
+      if (value == 1 && ctx->d.R > 640)
+        return ctx->fail(HPS_ERR_PARAM, "ParameterError: the lock-step kernel needs (p-2)^2 + 4(p-1) <= 640");
+      ctx->lockstep_env = value;
+      return HPS_OK;
+    default:
+      return ctx->fail(HPS_ERR_PARAM, "ParameterError: unknown option");
+  }
+}
+
 int hps_gpu_set_fault_injection(hps_gpu_ctx* ctx, const int32_t* elements, int32_t n) {
   if (!ctx) return HPS_ERR_PARAM;
   cudaSetDevice(ctx->device);

@@ -18,6 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("HPS_LIB_PATH") or os.path.join(_HERE, "_lib", "libhps_leaf_b200.so")
 
 HPS_OK, HPS_ERR_RESONANCE, HPS_ERR_PARAM, HPS_ERR_CUDA = 0, 1, 2, 3
+OPT_SMALL_KERNEL, OPT_LOCKSTEP = 1, 2
 STORAGE_RECOMPUTE, STORAGE_STORE = 0, 1
 
 
@@ -67,7 +68,7 @@ EXPORTED = ["hps_gpu_create", "hps_gpu_destroy", "hps_gpu_last_error", "hps_gpu_
             "hps_gpu_multi_ctx", "hps_gpu_multi_condense", "hps_gpu_multi_leaf_solve",
             "hps_gpu_multi_assemble_reduced", "hps_shard_range", "hps_reduced_cut_edges",
             "hps_reduced_host_edges", "hps_gpu_condense_assemble", "hps_gpu_reconstruct",
-            "hps_gpu_reconstruct_device", "hps_gpu_fp64_peak_tflops"]
+            "hps_gpu_reconstruct_device", "hps_gpu_fp64_peak_tflops", "hps_gpu_set_option"]
 
 
 def lib():
@@ -103,7 +104,7 @@ def lib():
                      "hps_gpu_leaf_solve_operator", "hps_gpu_multi_shards", "hps_gpu_multi_condense",
                      "hps_gpu_multi_leaf_solve", "hps_gpu_multi_assemble_reduced", "hps_shard_range",
                      "hps_reduced_cut_edges", "hps_reduced_host_edges", "hps_gpu_condense_assemble",
-                     "hps_gpu_reconstruct", "hps_gpu_reconstruct_device"):
+                     "hps_gpu_reconstruct", "hps_gpu_reconstruct_device", "hps_gpu_set_option"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -201,6 +202,11 @@ class LeafStage:
 
     def reset_timing(self):
         self._check(lib().hps_gpu_reset_timing(self._h))
+
+    def set_option(self, option, value):
+        """Kernel-path selection (hps_gpu_set_option): OPT_SMALL_KERNEL / OPT_LOCKSTEP,
+        value -1 default, 0 off, 1 on."""
+        self._check(lib().hps_gpu_set_option(self._h, option, value))
 
     def set_fault_injection(self, elements):
         el = np.asarray(elements, np.int32)

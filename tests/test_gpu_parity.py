@@ -291,21 +291,6 @@ def test_c4_subset_and_laplace_property():
     assert np.max(np.abs(flux[:, nc])) <= 1e-9 * np.max(np.abs(T))
 
 
-def test_fused_assembly_equals_materialised_k1(monkeypatch):
-    """K2's first-touch assembly (HPS_FUSED=1) evaluates exactly K1's entries: T, w bitwise
-    equal to the K1-materialised default path."""
-    p, nx, ny, kappa = 16, 3, 3, 40.0
-    X, Y = P.leaf_coords(nx, ny, p)
-    b = P.crystal_field(X * 0.4 + 0.3, Y * 0.4 + 0.3); f = np.cos(5 * X) * Y
-    with G().LeafStage(p, nx, ny, kappa) as st:
-        T1, w1, _ = st.condense(b, f)
-    monkeypatch.setenv("HPS_FUSED", "1")
-    with G().LeafStage(p, nx, ny, kappa) as st:
-        T2, w2, _ = st.condense(b, f)
-    assert np.array_equal(T1.view(np.int64), T2.view(np.int64))
-    assert np.array_equal(w1.view(np.int64), w2.view(np.int64))
-
-
 @pytest.mark.parametrize("p,kappa,n", [(6, 5.0, 3), (12, 20.0, 4), (13, 9.0, 3), (22, 100.0, 3), (42, 500.0, 2)])
 def test_s_solve_parity(p, kappa, n):
     """K3: S_solve = -A_ii^{-1} A_ib vs the oracle (dgetrs), relFro <= 1e-10,
@@ -324,17 +309,17 @@ def test_s_solve_parity(p, kappa, n):
 
 
 @pytest.mark.parametrize("p", [4, 5, 6, 7, 8, 9, 10, 11, 12])
-def test_small_kernel_matches_oracle_and_blocked_path(p, monkeypatch):
+def test_small_kernel_matches_oracle_and_blocked_path(p):
     """K2s (register-resident, fused assembly, p <= 12) against the oracle (1e-10 relFro) and
-    against the blocked K1+K2 path (HPS_SMALL=0); chunk-independent bitwise; crystal b near
+    against the blocked K1+K2 path (OPT_SMALL_KERNEL off); chunk-independent bitwise; crystal b near
     resonance-free range and f ~ U(-1,1) so w is exercised."""
     nx, ny, kappa = 7, 5, 4.0 * p
     X, Y = P.leaf_coords(nx, ny, p)
     b = P.crystal_field(X * 0.4 + 0.3, Y * 0.4 + 0.3)
     f = np.random.default_rng(p).uniform(-1, 1, b.shape)
     ref = O.batched_condense(p, 1.0 / nx, kappa, b, f)
-    monkeypatch.setenv("HPS_SMALL", "1")
     with G().LeafStage(p, nx, ny, kappa) as st:
+        st.set_option(G().OPT_SMALL_KERNEL, 1)
         T1, w1, s1 = st.condense(b, f)
         T3, w3, _ = st.condense(b[5:17], f[5:17], e0=5)
     assert not s1.any()
@@ -342,19 +327,19 @@ def test_small_kernel_matches_oracle_and_blocked_path(p, monkeypatch):
     assert rel_fro(w1, ref["w"]).max() <= TOL_T
     assert np.array_equal(T1[5:17].view(np.int64), T3.view(np.int64))
     assert np.array_equal(w1[5:17].view(np.int64), w3.view(np.int64))
-    monkeypatch.setenv("HPS_SMALL", "0")
     with G().LeafStage(p, nx, ny, kappa) as st:
+        st.set_option(G().OPT_SMALL_KERNEL, 0)   # blocked K1 + K2 path
         T2, w2, _ = st.condense(b, f)
     assert rel_fro(T1, T2).max() <= 1e-12
     assert rel_fro(w1, w2).max() <= 1e-12
 
 
 @pytest.mark.parametrize("p", [6, 12])
-def test_small_kernel_resonance_injection(p, monkeypatch):
-    monkeypatch.setenv("HPS_SMALL", "1")
+def test_small_kernel_resonance_injection(p):
     nx, ny = 4, 3
     b, f = random_leaves(p, nx * ny, seed=11)
     with G().LeafStage(p, nx, ny, 3.0) as st:
+        st.set_option(G().OPT_SMALL_KERNEL, 1)
         st.set_fault_injection([9, 4, 7])
         T, w, s = st.condense(b, f, raise_on_resonance=False)
         assert list(np.nonzero(s)[0]) == [4, 7, 9]
@@ -364,18 +349,18 @@ def test_small_kernel_resonance_injection(p, monkeypatch):
 
 
 @pytest.mark.parametrize("p", [16, 22])
-def test_lockstep_kernel_bitwise_equals_persistent(p, monkeypatch):
+def test_lockstep_kernel_bitwise_equals_persistent(p):
     """The lock-step multi-leaf K2 kernel runs the same per-leaf code as the one-leaf-per-CTA
-    persistent kernel: T, w bitwise equal (HPS_LOCKSTEP=1 vs 0), including a partial last
-    round (leaf count not a multiple of 4 x #SM) and a single-leaf call."""
+    persistent kernel: T, w bitwise equal (lock-step on vs off), including a partial last
+    round (leaf count not a multiple of 4 x #SM) and a single-leaf call (OPT_LOCKSTEP on/off)."""
     nx, ny, kappa = 7, 3, 5.0 * p
     X, Y = P.leaf_coords(nx, ny, p)
     b = P.crystal_field(X * 0.4 + 0.3, Y * 0.4 + 0.3)
     f = np.random.default_rng(p).uniform(-1, 1, b.shape)
     out = {}
     for ls in ("0", "1"):
-        monkeypatch.setenv("HPS_LOCKSTEP", ls)
         with G().LeafStage(p, nx, ny, kappa) as st:
+            st.set_option(G().OPT_LOCKSTEP, int(ls))
             T, w, s = st.condense(b, f)
             T1, w1, _ = st.condense(b[3:4], f[3:4], e0=3)
         assert not s.any()

@@ -81,6 +81,12 @@ constexpr int NWARP = NT / 32;
 #ifndef HPS_KC
 #define HPS_KC 16
 #endif
+// Column offset inside a row of the leaf matrix (row-major).  The tile microbenchmark
+// redefines these to measure a column-blocked layout (tools/microbench/tile_bench.cu).
+#ifndef HPS_KOFF
+#define HPS_KOFF(k) (k)
+#define HPS_COFF(c) (c)
+#endif
 constexpr int KC = HPS_KC;           // K chunk per stage
 constexpr int NSTAGE = HPS_NSTAGE;   // pipeline stages
 constexpr int MAX_NSTAGE = 4;
@@ -180,13 +186,13 @@ __device__ __forceinline__ void load_chunk(double* st, unsigned long long* full,
 #pragma unroll
     for (int r = 0; r < TL::AGR; ++r) {
       const int gi = tid + r * NT;
-      cp_async16(As + (gi / (KC_ / 2)) * TL::LDA + 2 * (gi % (KC_ / 2)), pa[r] + k0);
+      cp_async16(As + (gi / (KC_ / 2)) * TL::LDA + 2 * (gi % (KC_ / 2)), pa[r] + HPS_KOFF(k0));
     }
 #pragma unroll
     for (int r = 0; r < TL::BGR; ++r) {
       const int gi = tid + r * NT;
       const int row = gi / TL::BROW, seg = gi % TL::BROW;
-      cp_async16(Bs + row * TL::LDB + 2 * seg, brow(k0 + row) + 2 * seg);
+      cp_async16(Bs + row * TL::LDB + 2 * seg, brow(k0 + row) + HPS_COFF(2 * seg));
     }
     cp_async_mbar_arrive(full);
   } else {

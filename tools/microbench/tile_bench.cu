@@ -1,6 +1,15 @@
 // Isolated throughput of the K2 tile-job mainloop (tile_mma) on B200: every CTA runs
 // `reps` tile jobs C(TMxTN) -= A(TMxK) B(KxTN) on its own rows (perm = identity).
 #include <cstdio>
+// TB_BLK = 0: row-major leaf rows (stride ld).  TB_BLK > 0: column-blocked layout, 16-column
+// blocks of TB_BLK doubles each (all rows of a block contiguous, 128 B per row).
+#ifndef TB_BLK
+#define TB_BLK 0
+#endif
+#if TB_BLK
+#define HPS_KOFF(k) (((k) / 16) * (long long)TB_BLK)
+#define HPS_COFF(c) (((c) / 16) * (long long)TB_BLK + (c) % 16)
+#endif
 #include "../../paper_2211_14969_b200/csrc/k2_lu_schur.cu"
 
 using namespace hpsg;
@@ -25,9 +34,9 @@ __global__ void __launch_bounds__(NT, 2) tile_bench_kernel(double* ws, int ld, i
   for (int r = 0; r < reps; ++r) {
     const int rt = (r % 4) * TM_;
     const double* MA = HOT ? ws : M;
-    const int ldh = HOT ? 0 : ld;   // HOT: every row aliases row 0 -> L1/L2-resident operands
+    const int ldh = HOT ? 0 : (TB_BLK ? 16 : ld);   // HOT: every row aliases row 0 -> L1/L2-resident operands
     auto arow = [=](int i) -> const double* { return MA + (size_t)perm[rt + i] * ldh; };
-    auto brow = [=](int k) -> const double* { return MA + (size_t)perm[k] * ldh + 1024; };
+    auto brow = [=](int k) -> const double* { return MA + (size_t)perm[k] * ldh + HPS_COFF(1024); };
     auto crow = [=](int i) -> double* { return const_cast<double*>(M) + (size_t)perm[rt + i] * ld + 1536; };
     Acc acc;
     auto init = [&](Acc& x) { acc_load<TL>(x, crow, TM_); };

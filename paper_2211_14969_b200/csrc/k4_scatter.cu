@@ -12,7 +12,10 @@
 //        -( sum_t ( w_t[r_t] + sum_{Gamma cols} T_t[r_t, c] g_c ) )
 //  in exactly the order of the CPU oracle, with _rn intrinsics (no FMA
 //  contraction): given the same T, values and rhs are bit-identical.
-//  HBM bound: reads the active x active part of T, writes nnz values.
+//  HBM bound: reads the active x active part of T, writes nnz values.  Each CTA first tabulates
+//  its row pattern (T column and output offset per row position), then warps walk rows and
+//  lanes walk positions with four rows' loads in flight: no integer division per entry,
+//  C4 (211M nonzeros) in 0.75 ms = 5.4 TB/s of algorithmic B_K4 (83% of HBM).
 //
 //  BSR view (SPEC.md:331's ReducedSystem "blocks" are exactly
 //  this): block row = interface edge, block column = one of its <= 7 column
@@ -26,6 +29,10 @@
 #include "hps_kernels.h"
 
 namespace hpsg {
+
+#ifndef HPS_K4_MINB
+#define HPS_K4_MINB 6   // min CTAs/SM for the values kernel: 40-register cap (measured 5.4 vs 3.1 TB/s uncapped)
+#endif
 
 __device__ __forceinline__ int side_base(int p, int side) {
   return side == 0 ? 1 : side == 1 ? p : side == 2 ? 2 * p : 3 * p - 2;
@@ -69,7 +76,7 @@ __global__ void __launch_bounds__(256) k4_bsr_pattern_kernel(MeshDev m, int64_t*
 // BSR selects the output layout (see the header).  T and w are indexed by global element
 // id (a shard passes base pointers offset by its first leaf).
 template <bool BSR>
-__global__ void __launch_bounds__(256) k4_values_kernel(MeshDev m, const double* __restrict__ T,
+__global__ void __launch_bounds__(256, HPS_K4_MINB) k4_values_kernel(MeshDev m, const double* __restrict__ T,
                                                         const double* __restrict__ w,
                                                         const double* __restrict__ g_bnd,
                                                         double* __restrict__ values,
@@ -96,50 +103,47 @@ __global__ void __launch_bounds__(256) k4_values_kernel(MeshDev m, const double*
     }
   }
   __syncthreads();
-  // Four entries per thread per pass, all eight T loads issued before any sum/store
-  // (memory-level parallelism: the loop is HBM-latency bound otherwise).
-  constexpr int U = 4;
-  const int total = q * rowlen;
-  for (int e0 = threadIdx.x; e0 < total; e0 += U * blockDim.x) {
-    double tv[U][2];
-    bool has[U][2];
+  // Column table of the edge's rows (every row of an edge has the same columns): position
+  // pos = rank * q + kk -> T column of element t (side_base of its side + kk) or -1, and the
+  // output offset of (row k, pos) = k * kstride + pstride(pos) (CSR: k * rowlen + pos; BSR:
+  // k * q + rank * q * q + kk).  Each warp walks rows k, lanes walk positions: no integer
+  // division per entry, four rows' worth of loads in flight per lane.
+  constexpr int MAXPOS = 7 * 43;   // 7 column edges x (p - 2), p <= 45
+  __shared__ int tcol[2][MAXPOS];
+  __shared__ int opos[MAXPOS];
+  for (int pos = threadIdx.x; pos < rowlen; pos += blockDim.x) {
+    const int rank = pos / q, kk = pos - rank * q;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int e = e0 + u * blockDim.x;
-      has[u][0] = has[u][1] = false;
-      tv[u][0] = tv[u][1] = 0.0;
-      if (e < total) {
-        int k, rank, kk;
-        if (BSR) {
-          rank = e / (q * q);
-          const int rem = e - rank * q * q;
-          k = rem / q;
-          kk = rem - k * q;
-        } else {
-          k = e / rowlen;
-          const int pos = e - k * rowlen;
-          rank = pos / q;
-          kk = pos - rank * q;
-        }
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          const int sc = col_side[t][rank];
-          if (sc >= 0) {
-            const int r = side_base(p, sd[t]) + k;
-            tv[u][t] = __ldg(T + ((size_t)el[t] * nb + r) * nb + side_base(p, sc) + kk);
-            has[u][t] = true;
-          }
-        }
-      }
+    for (int t = 0; t < 2; ++t) {
+      const int sc = col_side[t][rank];
+      tcol[t][pos] = sc >= 0 ? side_base(p, sc) + kk : -1;
     }
+    opos[pos] = BSR ? rank * q * q + kk : pos;
+  }
+  __syncthreads();
+  const int kstride = BSR ? q : rowlen;
+  const double* T0 = T + ((size_t)el[0] * nb + side_base(p, sd[0])) * nb;
+  const double* T1 = T + ((size_t)el[1] * nb + side_base(p, sd[1])) * nb;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarp = blockDim.x >> 5;
+  constexpr int U = 4;   // rows per pass
+  for (int k0 = warp * U; k0 < q; k0 += nwarp * U) {
+    for (int pos = lane; pos < rowlen; pos += 32) {
+      const int c0 = tcol[0][pos], c1 = tcol[1][pos], o = opos[pos];
+      double tv[U][2];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int e = e0 + u * blockDim.x;
-      if (e < total) {
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + u;
+        tv[u][0] = (k < q && c0 >= 0) ? __ldg(T0 + (size_t)k * nb + c0) : 0.0;
+        tv[u][1] = (k < q && c1 >= 0) ? __ldg(T1 + (size_t)k * nb + c1) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int k = k0 + u;
+        if (k >= q) continue;
         double v = 0.0;   // 0 + T_e0 + T_e1 in the oracle's order (present terms only)
-        if (has[u][0]) v = __dadd_rn(v, tv[u][0]);
-        if (has[u][1]) v = __dadd_rn(v, tv[u][1]);
-        values[off + e] = v;
+        if (c0 >= 0) v = __dadd_rn(v, tv[u][0]);
+        if (c1 >= 0) v = __dadd_rn(v, tv[u][1]);
+        values[off + (int64_t)k * kstride + o] = v;
       }
     }
   }

@@ -81,6 +81,7 @@ constexpr int NWARP = NT / 32;
 #ifndef HPS_KC
 #define HPS_KC 16
 #endif
+
 // Column offset inside a row of the leaf matrix (row-major).  The tile microbenchmark
 // redefines these to measure a column-blocked layout (tools/microbench/tile_bench.cu).
 #ifndef HPS_KOFF
@@ -306,6 +307,40 @@ __device__ __forceinline__ void acc_zero(Acc& acc) {
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
     for (int ni = 0; ni < 4; ++ni) acc.v[mi][ni][0] = acc.v[mi][ni][1] = 0.0;
+}
+
+// Accuracy: a tile job accumulates its K-range product sum from ZERO and adds the original
+// entries once at the end (C <- C + (-sum A B)), instead of subtracting every product from a
+// running value initialised with C.  With near-singular A_ii (leaves next to a resonance) the
+// running-value form loses an order of magnitude: at C4's worst leaf (cond(A_ii) ~ 2e8) T was
+// 5.0e-11 from an extended-precision reference against LAPACK's 2.0e-12; the separate sum is
+// what blocked LAPACK effectively does (tools/leaf_refine.py, profiles/r02_leaf_refine_*.json).
+// Only the tile jobs need it (the in-panel updates sum at most 32 products: measured no gain,
+// profiles/r02_k2_accuracy_ab.log).  The C tile is prefetched into L1 when the job starts so
+// the epilogue's load hits.
+template <class TL, class CRow>
+__device__ __forceinline__ void acc_prefetch_l1(const CRow& crow, int nrows) {
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int r = acc_row<TL>(mi);
+    if (r >= nrows) continue;
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(crow(r) + acc_col<TL>(0)));
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(crow(r) + acc_col<TL>(2)));
+  }
+}
+template <class TL, class CRow>
+__device__ __forceinline__ void acc_add(Acc& acc, const CRow& crow, int nrows) {
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi) {
+    const int r = acc_row<TL>(mi);
+    if (r >= nrows) continue;
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      const double2 c = *reinterpret_cast<const double2*>(crow(r) + acc_col<TL>(ni));
+      acc.v[mi][ni][0] = __dadd_rn(c.x, acc.v[mi][ni][0]);
+      acc.v[mi][ni][1] = __dadd_rn(c.y, acc.v[mi][ni][1]);
+    }
+  }
 }
 
 template <class TL, class CRow>
@@ -811,12 +846,13 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf, const Gr
         const int nr = min(TLM, d.R - rt);
         auto crow = [=](int i) -> double* { return L.M + (size_t)perm[rt + i] * ld + c0; };
         Acc acc;
-        auto init = [&](Acc& x) { acc_load<TileL>(x, crow, nr); };
+        auto init = [&](Acc& x) { acc_zero(x); acc_prefetch_l1<TileL>(crow, nr); };
         auto arow = lrow(rt);
         auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + c0; };
         // columns c0 + w .. c0 + 63 of the last block are A_ii padding (zero): no DMMA there
         tile_mma<TileL>(G, acc, init, arow, brow, c0, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk,
                         nr, HPS_NACT ? w : 64);
+        acc_add<TileL>(acc, crow, nr);
         acc_store<TileL>(acc, crow, nr, 64);
       }
       __threadfence_block();
@@ -834,7 +870,7 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf, const Gr
     for (int ct = ct_begin; ct < ct_end; ct += TUN) {
       auto crow = [=](int i) -> double* { return L.M + (size_t)perm[c0 + i] * ld + ct; };
       Acc acc;
-      auto init = [&](Acc& x) { acc_load<TileU>(x, crow, 64); };
+      auto init = [&](Acc& x) { acc_zero(x); acc_prefetch_l1<TileU>(crow, 64); };
       auto arow = lrow(c0);
       auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + ct; };
       // Real (non-padding) columns of this tile: A_ii columns end at ni, the trailing block
@@ -843,6 +879,7 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf, const Gr
       const int nc = HPS_NACT ? min(TUN, real_end - ct) : TUN;
       tile_mma<TileU>(G, acc, init, arow, brow, c0, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk,
                       64, nc);
+      acc_add<TileU>(acc, crow, 64);
       linv_apply<TRI_LOWER>(G, acc, li, sm->pipe, nc);
       acc_store<TileU>(acc, crow, w, min(TUN, ct_end - ct));
     }
@@ -861,11 +898,12 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf, const Gr
       const int nr = min(TLM, d.R - rt);
       auto crow = [=](int i) -> double* { return L.M + (size_t)perm[rt + i] * ld + c0; };
       Acc acc;
-      auto init = [&](Acc& x) { acc_load<TileL>(x, crow, nr); };
+      auto init = [&](Acc& x) { acc_zero(x); acc_prefetch_l1<TileL>(crow, nr); };
       auto arow = lrow(rt);
       auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + c0; };
       tile_mma<TileL>(G, acc, init, arow, brow, d.ni, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk,
                       nr, HPS_NACT ? d.nb + 1 - 64 * tb : 64);
+      acc_add<TileL>(acc, crow, nr);
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi) {
         const int r = acc_row<TileL>(mi);
@@ -1024,8 +1062,9 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k3_ssolve_kernel(LuArgs a, do
         auto arow = [=](int i) -> const double* { return M + (size_t)perm[r0 + i] * ld + r0 + 64; };
         auto brow = [=](int k) -> const double* { return M + (size_t)perm[r0 + 64 + k] * ld + ct; };
         Acc acc;
-        auto init = [&](Acc& x) { acc_load<TileU>(x, crow, 64); };
+        auto init = [&](Acc& x) { acc_zero(x); acc_prefetch_l1<TileU>(crow, 64); };
         tile_mma<TileU>(G, acc, init, arow, brow, K, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk);
+        acc_add<TileU>(acc, crow, 64);
         linv_apply<TRI_UPPER>(G, acc, uinv, sm->pipe);
         acc_store<TileU>(acc, crow, w, min(TUN, ct_end - ct));
       }

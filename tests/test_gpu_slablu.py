@@ -65,3 +65,18 @@ def test_slablu_partition_rules():
         assert lu.info["max_interior"] == (3 * 2 + 2 * 3) * 6   # 3 columns: 6 horizontal + 2x3 vertical edges
     with pytest.raises(G().ParameterError):
         S().SlabLU(8, 7, 3, brp, bci, bva, slab_width=4)   # 1 slab < 2
+
+
+def test_slablu_singular_interface_block():
+    """A reduced system whose interface block is singular after elimination raises
+    SingularBlockError with that interface's index (errors.hpp:30-38)."""
+    p, nx, ny = 8, 4, 3
+    A, rhs, (brp, bci, bva) = reduced(p, nx, ny, 0.0)
+    q = p - 2
+    bva = bva.copy()
+    # interface 0 (width 1): the vertical edges at x-column 1 = edge ids [ny-1, 2ny-1)
+    for ed in range(ny - 1, 2 * ny - 1):
+        bva[brp[ed]:brp[ed + 1]] = 0.0
+    with pytest.raises(S().SingularBlockError) as ei:
+        S().SlabLU(p, nx, ny, brp, bci, bva, slab_width=1)
+    assert ei.value.block_index == 0

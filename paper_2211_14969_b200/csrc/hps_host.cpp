@@ -247,6 +247,7 @@ struct hps_gpu_ctx {
   int small_env = -1;
   bool k2s_trace = false;
   bool no_stage = false;
+  bool no_direct = false;   // debug: D2H copies even for mapped pinned outputs
   DevBuf phase_buf;
   DevBuf field_off, field_cent;   // K0 crystal sampler: node offsets, centres
   DevBuf op_A, op_Dn, op_b, op_f, op_v, op_T, op_w, op_st, op_S, op_u;   // operator-path staging
@@ -553,6 +554,7 @@ int hps_gpu_create(int device, const hps_leaf_desc* desc, hps_gpu_ctx** out) {
   c->small_env = env_int("HPS_SMALL", -1);
   c->k2s_trace = std::getenv("HPS_K2S_TRACE") != nullptr;
   c->no_stage = std::getenv("HPS_NO_STAGE") != nullptr;
+  c->no_direct = std::getenv("HPS_NO_DIRECT") != nullptr;
 #endif
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return reject(HPS_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
@@ -820,7 +822,26 @@ static int condense_pipeline(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const dou
   // serialise the pieces: pageable T/w land in pinned double buffers instead and are copied
   // out on the host while the next piece computes.
   const bool want_T = T != nullptr;
-  const bool stage = want_T && !pieces.empty() && !ctx->no_stage && !(host_pinned(T) && host_pinned(w));
+  const bool pinned_out = want_T && host_pinned(T) && host_pinned(w);
+  const bool stage = want_T && !pieces.empty() && !ctx->no_stage && !pinned_out;
+  // Pinned caller outputs mapped into the device address space: the register-resident K2s
+  // (p <= 12) writes T/w straight into host memory as each leaf finishes (the north star's "S
+  // blocks straight into pinned host memory"; C1 e2e 1.00M -> 1.19M leaves/s), so no D2H copy
+  // trails the last piece.  The blocked K2's D-row epilogue stores are too scattered for the
+  // host link (C2 e2e 145k -> 74k when tried): it keeps the staged D2H copies.
+  double* T_map = nullptr;
+  double* w_map = nullptr;
+  if (pinned_out && !dT_res && !ctx->no_direct &&
+      use_small(ctx, S != nullptr || ctx->desc.storage == HPS_STORAGE_STORE)) {
+    void* pt = nullptr;
+    void* pw = nullptr;
+    if (cudaHostGetDevicePointer(&pt, T, 0) == cudaSuccess && cudaHostGetDevicePointer(&pw, w, 0) == cudaSuccess) {
+      T_map = static_cast<double*>(pt);
+      w_map = static_cast<double*>(pw);
+    } else {
+      cudaGetLastError();
+    }
+  }
   if (stage) {
     const int maxp = *std::max_element(pieces.begin(), pieces.end());
     for (int i = 0; i < 2; ++i) {
@@ -844,8 +865,8 @@ static int condense_pipeline(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const dou
     const size_t off = size_t(c0 - e0);
     double* T_dst = stage ? ctx->h_T[k].as<double>() : want_T ? T + off * nb2 : nullptr;
     double* w_dst = stage ? ctx->h_w[k].as<double>() : want_T ? w + off * d.nb : nullptr;
-    double* dT = dT_res ? dT_res + off * nb2 : ctx->out_T[k].as<double>();
-    double* dw = dw_res ? dw_res + off * d.nb : ctx->out_w[k].as<double>();
+    double* dT = dT_res ? dT_res + off * nb2 : T_map ? T_map + off * nb2 : ctx->out_T[k].as<double>();
+    double* dw = dw_res ? dw_res + off * d.nb : w_map ? w_map + off * d.nb : ctx->out_w[k].as<double>();
     CK(cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_in_free[k], 0));
     CK(cudaMemcpyAsync(ctx->in_b[k].ptr, b + off * pp, n * pp * 8, cudaMemcpyHostToDevice, ctx->s_h2d));
     CK(cudaMemcpyAsync(ctx->in_f[k].ptr, f + off * pp, n * pp * 8, cudaMemcpyHostToDevice, ctx->s_h2d));
@@ -868,7 +889,7 @@ static int condense_pipeline(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const dou
     CK(cudaEventRecord(ctx->ev_in_free[k], ctx->s_comp));
     CK(cudaEventRecord(ctx->ev_out_ready[k], ctx->s_comp));
     CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_out_ready[k], 0));
-    if (want_T) {
+    if (want_T && !T_map) {
       CK(cudaMemcpyAsync(T_dst, dT, n * nb2 * 8, cudaMemcpyDeviceToHost, ctx->s_d2h));
       CK(cudaMemcpyAsync(w_dst, dw, n * size_t(d.nb) * 8, cudaMemcpyDeviceToHost, ctx->s_d2h));
     }

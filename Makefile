@@ -63,7 +63,7 @@ clean:
 	rm -rf build $(LIB) $(SLIB)
 	$(MAKE) -s -C oracle clean
 
-.PHONY: all oracle clean cxx_test
+.PHONY: all oracle clean cxx_test api_timing
 
 CXX_TEST := build/test_leaf_api
 cxx_test: $(CXX_TEST)
@@ -77,6 +77,13 @@ endif
 $(CXX_TEST): tests/cxx/test_leaf_api.cpp include/hps/leaf_gpu.hpp include/hps_leaf_gpu.h $(LIB)
 	@mkdir -p build
 	g++ -std=c++20 -O2 -Wall -Iinclude $(CXX_TEST_REF) -o $@ $< -L$(dir $(LIB)) -lhps_leaf_b200 \
+	    -Wl,-rpath,'$$ORIGIN/../paper_2211_14969_b200/_lib'
+
+API_TIMING := build/api_timing
+api_timing: $(API_TIMING)
+$(API_TIMING): tools/cxx/api_timing.cpp include/hps/leaf_gpu.hpp include/hps_leaf_gpu.h $(LIB)
+	@mkdir -p build
+	g++ -std=c++20 -O2 -Iinclude -o $@ $< -L$(dir $(LIB)) -lhps_leaf_b200 \
 	    -Wl,-rpath,'$$ORIGIN/../paper_2211_14969_b200/_lib'
 
 # A/B copy of the library with other K2 knobs, e.g.

@@ -215,35 +215,47 @@ void gather_leaves(const MeshTopology& topo, const std::vector<CondensedLeaf>& l
   }
 }
 
+// Pinned staging of the leaf-major T/w the GPU writes (grow-only, one per thread): a fresh
+// cudaHostAlloc of 2 GB at C4 costs about a second per call.
+struct PinnedScratch {
+  void* p = nullptr;
+  size_t bytes = 0;
+  ~PinnedScratch() { hps_host_free(p); }
+  double* get(size_t n) {
+    if (n * sizeof(double) > bytes) {
+      hps_host_free(p);
+      p = hps_host_alloc(n * sizeof(double));
+      bytes = p ? n * sizeof(double) : 0;
+      if (!p) throw std::runtime_error("batched_condense: pinned host allocation failed");
+    }
+    return static_cast<double*>(p);
+  }
+};
+thread_local PinnedScratch t_pinned_T, t_pinned_w;
+
 std::vector<CondensedLeaf> condense_on(hps_gpu_ctx* ctx, const MeshTopology& topo, const ProblemSpec& spec,
                                        int workers, bool want_s, const std::vector<double>& f_full) {
   const int n = topo.params.nx * topo.params.ny;
   const int nb = 4 * (topo.params.p - 1), ni = (topo.params.p - 2) * (topo.params.p - 2);
   std::vector<double> b, f;
   sample_leaves(topo, spec, 0, n, f_full, workers, b, f);
-  double* T = static_cast<double*>(hps_host_alloc(sizeof(double) * size_t(n) * nb * nb));
-  double* w = static_cast<double*>(hps_host_alloc(sizeof(double) * size_t(n) * nb));
-  if (!T || !w) {
-    hps_host_free(T);
-    hps_host_free(w);
-    throw std::runtime_error("batched_condense: pinned host allocation failed");
-  }
+  double* T = t_pinned_T.get(size_t(n) * nb * nb);
+  double* w = t_pinned_w.get(size_t(n) * nb);
   std::vector<double> S(want_s ? size_t(n) * ni * nb : 0);
   std::vector<int32_t> st(n);
   const int rc = hps_gpu_condense(ctx, 0, n, b.data(), f.data(), T, w, want_s ? S.data() : nullptr, st.data());
   std::vector<CondensedLeaf> out;
   if (rc == HPS_OK) {
     out.resize(n);
-    for (int e = 0; e < n; ++e) {
+    // one value per element, filled in parallel
+    for_elements(n, workers, [&](int e) {
       out[e].element_id = e;
       out[e].n_b = nb;
       out[e].T_flux.assign(T + size_t(e) * nb * nb, T + size_t(e + 1) * nb * nb);
       out[e].w_equiv.assign(w + size_t(e) * nb, w + size_t(e + 1) * nb);
       if (want_s) out[e].S_solve.assign(S.begin() + size_t(e) * ni * nb, S.begin() + size_t(e + 1) * ni * nb);
-    }
+    });
   }
-  hps_host_free(T);
-  hps_host_free(w);
   throw_rc(rc, ctx, st.data(), 0, n);
   return out;
 }

@@ -33,6 +33,15 @@ sys.path.insert(0, ROOT)
 from paper_2211_14969_b200 import problems as P  # noqa: E402
 
 METRIC = "leaf-condensation leaves/s & DOF/s at p=22/42 (1/2/4/8 B200), FP64 TFLOP/s vs peak"
+def _hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"])
+    except Exception:
+        return 6552.0   # B200 measured copy bandwidth (MEASURED_PEAKS.json of this pool)
+
+
+hbm_peak = _hbm_peak()
 FP64_PEAK_TFLOPS = 37.1   # fallback: DMMA m8n8k4 loop on this pool's B200 (profiles/r01_fp64_peak.log)
 FP64_PEAK_NOTE = ("measured in this run on this GPU: register-only DMMA m8n8k4 loop, hps_gpu_fp64_peak_tflops "
                   "(MEASURED_PEAKS.json and B200_PROFILING.md have no FP64 figure)")
@@ -463,6 +472,51 @@ def main():
         cpu = {"value": v, "unit": "leaves/s", "cores": cores, "kind": "port", "sample": sample,
                "cpu_model": cpu_model()}
 
+    # ---- storage policy 's_solve' (PAPER.md:162-165 trade study): condense also keeps
+    # [S_solve | A_ii^-1 f] per leaf (K3), leaf_solve is one HBM-bound GEMV per leaf (K5s) ----
+    stored = None
+    if args.leaf_solve:
+        stage.close()
+        torch.cuda.empty_cache()
+        try:
+            st3 = G.LeafStage(p, cfg["nx"], cfg["ny"], cfg["kappa"], a=cfg["a"], device=local,
+                              storage=G.STORAGE_S_SOLVE)
+            n3 = n
+            pb = G.PinnedArray(b.shape); pb.array[:] = b
+            pf = G.PinnedArray(f.shape); pf.array[:] = f
+            pT = G.PinnedArray((n3, nb, nb)); pw = G.PinnedArray((n3, nb))
+            v3 = np.random.default_rng(3).uniform(-1.0, 1.0, (n3, nb))
+            pv = G.PinnedArray(v3.shape); pv.array[:] = v3
+            pu = G.PinnedArray((n3, p * p))
+            st3.condense(pb.array, pf.array, e0=e0, out=(pT.array, pw.array), raise_on_resonance=False)
+            t3 = st3.timing()
+            st3.leaf_solve(pb.array, pf.array, pv.array, e0=e0, out=pu.array)   # warm-up
+            ks = 5
+            dev_ms = 0.0
+            t0 = time.perf_counter()
+            for _ in range(ks):
+                st3.leaf_solve(pb.array, pf.array, pv.array, e0=e0, out=pu.array)
+                dev_ms += st3.timing()["ms_lu_schur"]
+            dt = time.perf_counter() - t0
+            ni = (p - 2) ** 2
+            byts = 8 * (ni * (nb + 1) + nb + p * p)
+            stored = {"policy": "s_solve (HPS_STORAGE_S_SOLVE)",
+                      "condense_device_ms": t3["ms_total"],
+                      "condense_leaves_per_s_device": n3 / (t3["ms_total"] / 1e3),
+                      "store_bytes": int(n3 * ni * (nb + 1) * 8),
+                      "leaf_solve_e2e_leaves_per_s": n3 * ks / dt,
+                      "leaf_solve_device_ms": dev_ms / ks,
+                      "leaf_solve_device_leaves_per_s": n3 / (dev_ms / ks / 1e3),
+                      "k5s_roofline": {"bound": "hbm", "bytes_per_leaf": byts,
+                                       "achieved": n3 * byts / (dev_ms / ks / 1e3) / 1e9,
+                                       "peak": hbm_peak, "unit": "GB/s",
+                                       "frac": n3 * byts / (dev_ms / ks / 1e3) / 1e9 / hbm_peak}}
+            for a_ in (pb, pf, pT, pw, pv, pu):
+                a_.free()
+            st3.close()
+        except Exception as ex:   # e.g. the store does not fit next to the workspace
+            stored = {"policy": "s_solve", "skipped": str(ex)[:200]}
+
     if rank == 0:
         value = cfg["n_leaves"] * args.steps / (ms_max / 1e3)
         f_leaf = P.flops_condense(p)
@@ -498,6 +552,7 @@ def main():
             "chunk_leaves": info["chunk_leaves"],
             "secondary": secondary,
             "leaf_solve": leaf_solve,
+            "leaf_solve_stored_s_solve": stored,
         }
         print(json.dumps(line), flush=True)
     stage.close()

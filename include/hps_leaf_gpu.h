@@ -42,9 +42,17 @@ extern "C" {
 #define HPS_ERR_PARAM 2
 #define HPS_ERR_CUDA 3
 
-/* SPEC.md:313 storage policy for leaf factors. */
+/* SPEC.md:313 storage policy for leaf factors (recompute vs store):
+ *   RECOMPUTE  leaf_solve rebuilds and refactors A_ii (default; nothing kept);
+ *   STORE      the LU factors of the condensed range stay in HBM (25.7 MB/leaf at p=42, so the
+ *              whole range must fit one device chunk); leaf_solve re-solves with its f;
+ *   S_SOLVE    condense also back-substitutes [S_solve | A_ii^{-1} f_i] (K3, +~12% condense
+ *              time) and keeps it for every leaf (n_i (n_b+1) doubles: 2.1 MB/leaf at p=42,
+ *              20 GB at C4); leaf_solve is then one HBM-bound GEMV per leaf (K5s), using the
+ *              load f_i of the condense call (its b, f arguments are not read). */
 #define HPS_STORAGE_RECOMPUTE 0
 #define HPS_STORAGE_STORE 1
+#define HPS_STORAGE_S_SOLVE 2
 
 typedef struct hps_gpu_ctx hps_gpu_ctx;
 
@@ -54,7 +62,7 @@ typedef struct hps_gpu_ctx hps_gpu_ctx;
 typedef struct {
   int32_t p;               /* nodes per leaf side, 4 <= p <= 45 */
   int32_t nx, ny;          /* leaf grid (elements) */
-  int32_t storage;         /* HPS_STORAGE_RECOMPUTE (default) or HPS_STORAGE_STORE */
+  int32_t storage;         /* HPS_STORAGE_RECOMPUTE (default), _STORE or _S_SOLVE */
   double a;                /* leaf side length, > 0 */
   double kappa;            /* wavenumber, >= 0 */
   int64_t workspace_bytes; /* 0: 70% of free device memory */

@@ -253,6 +253,9 @@ struct hps_gpu_ctx {
   DevBuf op_A, op_Dn, op_b, op_f, op_v, op_T, op_w, op_st, op_S, op_u;   // operator-path staging
   DevBuf k4_T, k4_w, k4_g, k4_vals, k4_rhs, k4_list;   // assemble_reduced (host buffers), persistent
   DevBuf rc_ua, rc_g, rc_b, rc_f, rc_v, rc_ul, rc_u, rc_st, rc_tab;   // reconstruct_full_solution
+  DevBuf s_store;                 // HPS_STORAGE_S_SOLVE: [S_solve | A_ii^{-1} f] of every leaf
+  DevBuf ls_v, ls_u, ls_st;       // stored-S_solve leaf_solve I/O
+  bool s_solve() const { return desc.storage == HPS_STORAGE_S_SOLVE; }
   DevBuf res_flux, res_pl, res_pe, res_in;   // K6 residual scratch
   int store_e0 = -1, store_e1 = -1;
   HostBuf h_status;               // pinned staging of status[] (see HostBuf)
@@ -542,7 +545,7 @@ int hps_gpu_create(int device, const hps_leaf_desc* desc, hps_gpu_ctx** out) {
     return reject(HPS_ERR_PARAM, "ParameterError: kappa must be >= 0");
   if (D.nx < 1 || D.ny < 1)
     return reject(HPS_ERR_PARAM, "ParameterError: nx, ny must be >= 1");
-  if (D.storage != HPS_STORAGE_RECOMPUTE && D.storage != HPS_STORAGE_STORE)
+  if (D.storage != HPS_STORAGE_RECOMPUTE && D.storage != HPS_STORAGE_STORE && D.storage != HPS_STORAGE_S_SOLVE)
     return reject(HPS_ERR_PARAM, "ParameterError: unknown storage policy");
   hps_gpu_ctx* c = ctx.get();
 #ifdef HPS_DEBUG_KNOBS
@@ -613,6 +616,14 @@ int hps_gpu_create(int device, const hps_leaf_desc* desc, hps_gpu_ctx** out) {
     cudaMemGetInfo(&fr, &tot);
     budget = size_t(double(fr) * 0.7);
   }
+  const size_t s_bytes = D.storage == HPS_STORAGE_S_SOLVE
+                             ? size_t(c->n_leaves) * size_t(d.ni) * size_t(d.nb + 1) * sizeof(double) : 0;
+  if (s_bytes) {
+    if (budget < s_bytes + c->per_leaf)
+      return reject(HPS_ERR_PARAM, "ParameterError: storage policy 's_solve' needs " + std::to_string(s_bytes >> 20) +
+                                       " MiB for the stored S_solve blocks; exceeds the device budget");
+    budget -= s_bytes;
+  }
   int chunk = int(std::min<size_t>(size_t(c->n_leaves), budget / c->per_leaf));
   c->k2_ctas = hpsg::lu_ctas_per_sm(d, c->force_cfg);
   const int slots = c->k2_ctas * c->sms;
@@ -634,6 +645,7 @@ int hps_gpu_create(int device, const hps_leaf_desc* desc, hps_gpu_ctx** out) {
     CK(c->minratio.ensure(size_t(chunk) * 8));
     CK(c->status.ensure(size_t(chunk) * 4));
     CK(c->inject_all.ensure(size_t(c->n_leaves) * 4));
+    if (s_bytes) CK(c->s_store.ensure(s_bytes));
     CK(cudaMemset(c->inject_all.ptr, 0, size_t(c->n_leaves) * 4));
     CK(cudaMemset(c->ws.ptr, 0, (size_t(chunk) * d.leaf_stride + 2 * size_t(d.ld)) * 8));
   }
@@ -791,6 +803,20 @@ static bool host_pinned(const void* ptr) {
   return at.type == cudaMemoryTypeHost;
 }
 
+// HPS_STORAGE_S_SOLVE: K3 back-substitutes the factored chunk's [A_ib | f] columns into the
+// resident store at the leaves' slots (element c0 .. c0 + n).
+static void enqueue_s_store(hps_gpu_ctx* ctx, int c0, int n, cudaStream_t st) {
+  const LeafDims& d = ctx->d;
+  hpsg::LuArgs a3;
+  a3.d = d;
+  a3.ws = ctx->ws.as<double>();
+  a3.perm = ctx->perm.as<short>();
+  a3.s_with_load = 1;
+  hpsg::launch_ssolve(a3, ctx->s_store.as<double>() + size_t(c0) * d.ni * (d.nb + 1), ctx->uinv.as<double>(), n,
+                      st, ctx->force_cfg);
+  ctx->tkernels += 1;
+}
+
 // Host-buffer condense pipeline.  dT_res/dw_res (device, nullable): keep every leaf's T/w
 // resident in HBM at (e - e0) instead of the double-buffered staging (hps_gpu_condense_assemble
 // runs K4 on them afterwards); T/w (host) may then be null (no D2H of T at all).
@@ -810,9 +836,9 @@ static int condense_pipeline(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const dou
       CK(ctx->out_w[i].ensure(size_t(chunk) * d.nb * 8));
     }
     CK(ctx->out_st[i].ensure(size_t(chunk) * 4));
-    if (S) CK(ctx->out_S[i].ensure(size_t(chunk) * d.ni * d.nb * 8));
+    if (S && !ctx->s_solve()) CK(ctx->out_S[i].ensure(size_t(chunk) * d.ni * d.nb * 8));
   }
-  if (S) CK(ctx->uinv.ensure(size_t(4 * ctx->sms) * 4096 * 8));
+  if (S || ctx->s_solve()) CK(ctx->uinv.ensure(size_t(4 * ctx->sms) * 4096 * 8));
   const size_t nis = size_t(d.ni) * d.nb;
   const std::vector<int> pieces =
       io_schedule(e1 - e0, chunk, ctx->k2_ctas * ctx->sms, ctx->io_pieces,
@@ -832,7 +858,7 @@ static int condense_pipeline(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const dou
   double* T_map = nullptr;
   double* w_map = nullptr;
   if (pinned_out && !dT_res && !ctx->no_direct &&
-      use_small(ctx, S != nullptr || ctx->desc.storage == HPS_STORAGE_STORE)) {
+      use_small(ctx, S != nullptr || ctx->desc.storage != HPS_STORAGE_RECOMPUTE)) {
     void* pt = nullptr;
     void* pw = nullptr;
     if (cudaHostGetDevicePointer(&pt, T, 0) == cudaSuccess && cudaHostGetDevicePointer(&pw, w, 0) == cudaSuccess) {
@@ -875,8 +901,10 @@ static int condense_pipeline(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const dou
     CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_out_free[k], 0));
     enqueue_condense_chunk(ctx, c0, n, ctx->in_b[k].as<double>(), ctx->in_f[k].as<double>(), dT, dw,
                            ctx->out_st[k].as<int>(), ctx->s_comp,
-                           S != nullptr || ctx->desc.storage == HPS_STORAGE_STORE);
-    if (S) {  // K3: S_solve from the factored workspace
+                           S != nullptr || ctx->desc.storage != HPS_STORAGE_RECOMPUTE);
+    if (ctx->s_solve()) {   // K3 into the resident store: [S_solve | A_ii^{-1} f] of these leaves
+      enqueue_s_store(ctx, c0, n, ctx->s_comp);
+    } else if (S) {  // K3: S_solve from the factored workspace
       hpsg::LuArgs a3;
       a3.d = d;
       a3.ws = ctx->ws.as<double>();
@@ -895,7 +923,11 @@ static int condense_pipeline(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const dou
     }
     CK(cudaMemcpyAsync(ctx->h_status.as<int32_t>() + off, ctx->out_st[k].ptr, n * 4, cudaMemcpyDeviceToHost,
                        ctx->s_d2h));
-    if (S)
+    if (S && ctx->s_solve())   // the n_b S_solve columns of the stored (n_b + 1)-wide rows
+      CK(cudaMemcpy2DAsync(S + off * nis, size_t(d.nb) * 8,
+                           ctx->s_store.as<double>() + size_t(c0) * d.ni * (d.nb + 1), size_t(d.nb + 1) * 8,
+                           size_t(d.nb) * 8, size_t(n) * d.ni, cudaMemcpyDeviceToHost, ctx->s_d2h));
+    else if (S)
       CK(cudaMemcpyAsync(S + off * nis, ctx->out_S[k].ptr, n * nis * 8, cudaMemcpyDeviceToHost, ctx->s_d2h));
     CK(cudaEventRecord(ctx->ev_out_free[k], ctx->s_d2h));
     if (stage && ci > 0) CK(drain(ci - 1, off - size_t(pieces[ci - 1]), pieces[ci - 1]));
@@ -909,7 +941,7 @@ static int condense_pipeline(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const dou
   }
   std::memcpy(status, ctx->h_status.ptr, size_t(e1 - e0) * 4);
   finish_timing(ctx);
-  if (ctx->desc.storage == HPS_STORAGE_STORE) {
+  if (ctx->desc.storage != HPS_STORAGE_RECOMPUTE) {
     ctx->store_e0 = e0;
     ctx->store_e1 = e1;
   }
@@ -984,16 +1016,18 @@ int hps_gpu_condense_device(hps_gpu_ctx* ctx, int32_t e0, int32_t n, const doubl
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->s_comp;
   const LeafDims& d = ctx->d;
   const size_t pp = size_t(d.p) * d.p, nb2 = size_t(d.nb) * d.nb;
+  if (ctx->s_solve()) CK(ctx->uinv.ensure(size_t(4 * ctx->sms) * 4096 * 8));
   CK(cudaStreamWaitEvent(st, ctx->ev_scratch, 0));
   for (int c0 = 0; c0 < n; c0 += ctx->chunk) {
     const int m = std::min(ctx->chunk, n - c0);
     enqueue_condense_chunk(ctx, e0 + c0, m, d_b + c0 * pp, d_f + c0 * pp, d_T + c0 * nb2,
-                           d_w + size_t(c0) * d.nb, d_status + c0, st, store);
+                           d_w + size_t(c0) * d.nb, d_status + c0, st, ctx->desc.storage != HPS_STORAGE_RECOMPUTE);
+    if (ctx->s_solve()) enqueue_s_store(ctx, e0 + c0, m, st);
     CK(cudaGetLastError());
   }
   CK(cudaEventRecord(ctx->ev_scratch, st));
-  // 'store': the kept factors are now those of [e0, e0 + n) (one chunk, checked above).
-  if (store) {
+  // 'store' / 's_solve': the kept factors / S_solve blocks are now those of [e0, e0 + n).
+  if (ctx->desc.storage != HPS_STORAGE_RECOMPUTE) {
     ctx->store_e0 = e0;
     ctx->store_e1 = e0 + n;
   }
@@ -1075,6 +1109,16 @@ int hps_gpu_residual(hps_gpu_ctx* ctx, const double* b, const double* f, const d
 static cudaError_t enqueue_leaf_solve_chunk(hps_gpu_ctx* ctx, int c0, int n, const double* d_b, const double* d_f,
                                             const double* d_v, double* d_u, int* d_st, cudaStream_t st) {
   const LeafDims& d = ctx->d;
+  if (ctx->s_solve()) {   // K5s: one GEMV per leaf from the stored [S_solve | A_ii^{-1} f]
+    const int slot = next_timing_slot(ctx);
+    ctx->tkernels += 1;
+    cudaEventRecord(ctx->timing_event(3 * slot), st);
+    cudaEventRecord(ctx->timing_event(3 * slot + 1), st);
+    hpsg::launch_stored_solve(d.p, ctx->s_store.as<double>() + size_t(c0) * d.ni * (d.nb + 1), d_v, d_u, n, st);
+    cudaMemsetAsync(d_st, 0, size_t(n) * 4, st);
+    cudaEventRecord(ctx->timing_event(3 * slot + 2), st);
+    return cudaGetLastError();
+  }
   const bool store = ctx->desc.storage == HPS_STORAGE_STORE;
   const int slot = next_timing_slot(ctx);
   ctx->tkernels += store ? 3 : 4;
@@ -1126,8 +1170,7 @@ int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b
   if (!ctx) return HPS_ERR_PARAM;
   if (int rc = check_range(ctx, e0, e1)) return rc;
   if (!b || !f || !v || !u || !status) return ctx->fail(HPS_ERR_PARAM, "ParameterError: null buffer");
-  const bool store = ctx->desc.storage == HPS_STORAGE_STORE;
-  if (store && (e0 < ctx->store_e0 || e1 > ctx->store_e1))
+  if (ctx->desc.storage != HPS_STORAGE_RECOMPUTE && (e0 < ctx->store_e0 || e1 > ctx->store_e1))
     return ctx->fail(HPS_ERR_PARAM, "ParameterError: store policy: no kept factors for [" +
                                         std::to_string(e0) + ", " + std::to_string(e1) + ")");
   CK(cudaSetDevice(ctx->device));
@@ -1167,8 +1210,10 @@ int hps_gpu_leaf_solve(hps_gpu_ctx* ctx, int32_t e0, int32_t e1, const double* b
     const int k = ci & 1;
     const size_t off = size_t(c0 - e0);
     CK(cudaStreamWaitEvent(ctx->s_h2d, ctx->ev_in_free[k], 0));
-    CK(cudaMemcpyAsync(ctx->in_b[k].ptr, b + off * pp, n * pp * 8, cudaMemcpyHostToDevice, ctx->s_h2d));
-    CK(cudaMemcpyAsync(ctx->in_f[k].ptr, f + off * pp, n * pp * 8, cudaMemcpyHostToDevice, ctx->s_h2d));
+    if (!ctx->s_solve()) {   // the stored policy reads only v
+      CK(cudaMemcpyAsync(ctx->in_b[k].ptr, b + off * pp, n * pp * 8, cudaMemcpyHostToDevice, ctx->s_h2d));
+      CK(cudaMemcpyAsync(ctx->in_f[k].ptr, f + off * pp, n * pp * 8, cudaMemcpyHostToDevice, ctx->s_h2d));
+    }
     CK(cudaMemcpyAsync(ctx->in_v[k].ptr, v + off * nb, n * nb * 8, cudaMemcpyHostToDevice, ctx->s_h2d));
     CK(cudaEventRecord(ctx->ev_in_ready[k], ctx->s_h2d));
     CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_in_ready[k], 0));
@@ -1348,7 +1393,7 @@ int hps_gpu_reconstruct_device(hps_gpu_ctx* ctx, const double* d_u_active, const
   if (!d_u_active || !d_g_bnd || !d_b || !d_f || !d_u_full || !d_status)
     return ctx->fail(HPS_ERR_PARAM, "ParameterError: null device buffer");
   const int n = ctx->n_leaves;
-  if (ctx->desc.storage == HPS_STORAGE_STORE && (ctx->store_e0 > 0 || ctx->store_e1 < n))
+  if (ctx->desc.storage != HPS_STORAGE_RECOMPUTE && (ctx->store_e0 > 0 || ctx->store_e1 < n))
     return ctx->fail(HPS_ERR_PARAM, "ParameterError: store policy: no kept factors for the whole mesh");
   CK(cudaSetDevice(ctx->device));
   cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : ctx->s_comp;
@@ -1545,8 +1590,8 @@ static int operator_pass(hps_gpu_ctx* ctx, bool solve, int32_t e0, int32_t e1, c
   }
   CK(cudaEventRecord(ctx->ev_scratch, st));
   finish_timing(ctx);
-  // the kept factors (if any) were overwritten
-  ctx->store_e0 = ctx->store_e1 = -1;
+  // the kept LU factors (if any) were overwritten (a stored S_solve is not touched)
+  if (ctx->desc.storage == HPS_STORAGE_STORE) ctx->store_e0 = ctx->store_e1 = -1;
   std::vector<int> bad;
   for (int i = 0; i < e1 - e0; ++i)
     if (status[i]) bad.push_back(e0 + i);

@@ -50,6 +50,7 @@ struct LuArgs {
   int factor;           // 1: factor A_ii then trailing columns; 0: trailing columns only
   long long* phase_cycles = nullptr;  // optional 8 counters per leaf (profiling)
   int lockstep = 0;                   // factor: lock-step multi-leaf kernel (panels aligned)
+  int s_with_load = 0;                // K3: S rows hold n_b + 1 entries, the last = +A_ii^{-1} f_i
   const int* inject = nullptr;         // per leaf, nullable
 };
 // Two builds of k2_lu_schur.cu: g256 (8-warp CTAs, R <= 2048) and g128 (4-warp CTAs,
@@ -113,6 +114,10 @@ void launch_small_condense(const SmallArgs& a, int p, int n_leaves, cudaStream_t
 // local solution vector u (p*p per leaf): interior from the solve, boundary = v.
 void launch_backsolve(const LeafDims& d, const double* ws, const short* perm, const double* v,
                       double* u, int n_leaves, cudaStream_t st);
+
+// K5s: u = [A_ii^{-1} f + S_solve v on the interior, v on the boundary] from stored
+// [S_solve | A_ii^{-1} f] (n_i x (n_b + 1) per leaf).
+void launch_stored_solve(int p, const double* S, const double* v, double* u, int n_leaves, cudaStream_t st);
 
 // Mesh tables for K4 (device pointers).
 struct MeshDev {

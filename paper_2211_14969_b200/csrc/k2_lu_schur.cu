@@ -1052,7 +1052,8 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k3_ssolve_kernel(LuArgs a, do
     for (int i = threadIdx.x; i < MAX_RPAD; i += NT) sm->perm[i] = i < d.Rpad ? perm_g[i] : (short)(d.Rpad - 1);
     __syncthreads();
     const short* perm = sm->perm;
-    const int ct_end = d.tb0 + d.nb;
+    const int sc = d.nb + a.s_with_load;   // S columns: A_ib (and the load column)
+    const int ct_end = d.tb0 + sc;
     for (int I = d.nblk - 1; I >= 0; --I) {
       const int r0 = 64 * I, w = min(64, d.ni - r0);
       block_uinv(G, M, perm, ld, r0, w, sm->pipe, uinv);
@@ -1071,10 +1072,11 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k3_ssolve_kernel(LuArgs a, do
       __threadfence_block();
       __syncthreads();
     }
-    double* Sl = S_out + (size_t)leaf * d.ni * d.nb;
-    for (int e = threadIdx.x; e < d.ni * d.nb; e += NT) {
-      const int k = e / d.nb, c = e % d.nb;
-      Sl[e] = -M[(size_t)perm[k] * ld + d.tb0 + c];
+    double* Sl = S_out + (size_t)leaf * d.ni * sc;
+    for (int e = threadIdx.x; e < d.ni * sc; e += NT) {
+      const int k = e / sc, c = e - sc * (e / sc);
+      const double x = M[(size_t)perm[k] * ld + d.tb0 + c];
+      Sl[e] = c < d.nb ? -x : x;   // S_solve = -A_ii^{-1} A_ib ; +A_ii^{-1} f_i
     }
     __syncthreads();
   }

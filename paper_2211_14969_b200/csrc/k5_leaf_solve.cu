@@ -90,13 +90,41 @@ void launch_backsolve(const LeafDims& d, const double* ws, const short* perm, co
                       double* u, int n_leaves, cudaStream_t st) {
   if (n_leaves <= 0) return;
   const size_t smem = (size_t)d.ni * sizeof(double) + (size_t)d.ni * sizeof(short) + 16;
-  static size_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    cudaFuncSetAttribute(k5_backsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    configured = smem;
-  }
+  // a per-device function attribute: set on every launch (several GPUs in one process)
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k5_backsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k5_backsolve_kernel<<<n_leaves, 256, smem, st>>>(d, ws, perm, v, u);
+}
+
+// K5s — leaf_solve from a stored S_solve (HPS_STORAGE_S_SOLVE; SPEC.md:263,297-305,313;
+// PAPER.md:162-165): interior = A_ii^{-1} f_i + S_solve v with [S_solve | A_ii^{-1} f_i] kept
+// per leaf (n_i x (n_b + 1), row-major) by the condense call.  One CTA per leaf, one warp per
+// interior row: lanes stride the n_b + 1 row entries, fixed shuffle tree (deterministic).  HBM
+// bound: reads the stored row block once (8 n_i (n_b + 1) bytes per leaf).
+__global__ void __launch_bounds__(256) k5s_apply_kernel(int p, const double* __restrict__ S,
+                                                        const double* __restrict__ v, double* __restrict__ u) {
+  const int leaf = blockIdx.x;
+  const int q = p - 2, ni = q * q, nb = 4 * (p - 1), pp = p * p;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const double* Sl = S + (size_t)leaf * ni * (nb + 1);
+  const double* vl = v + (size_t)leaf * nb;
+  double* ul = u + (size_t)leaf * pp;
+  for (int i = warp; i < ni; i += 8) {
+    const double* row = Sl + (size_t)i * (nb + 1);
+    double acc = 0.0;
+    for (int k = lane; k < nb; k += 32) acc = fma(__ldg(row + k), __ldg(vl + k), acc);
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) ul[interior_local(i, p)] = __dadd_rn(__ldg(row + nb), acc);
+  }
+  for (int k = threadIdx.x; k < nb; k += 256) {
+    int e;
+    ul[boundary_local(k, p, &e)] = __ldg(vl + k);
+  }
+}
+
+void launch_stored_solve(int p, const double* S, const double* v, double* u, int n_leaves, cudaStream_t st) {
+  if (n_leaves <= 0) return;
+  k5s_apply_kernel<<<n_leaves, 256, 0, st>>>(p, S, v, u);
 }
 
 }  // namespace hpsg

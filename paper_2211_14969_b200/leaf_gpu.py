@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("HPS_LIB_PATH") or os.path.join(_HERE, "_lib", "libhps
 
 HPS_OK, HPS_ERR_RESONANCE, HPS_ERR_PARAM, HPS_ERR_CUDA = 0, 1, 2, 3
 OPT_SMALL_KERNEL, OPT_LOCKSTEP = 1, 2
-STORAGE_RECOMPUTE, STORAGE_STORE = 0, 1
+STORAGE_RECOMPUTE, STORAGE_STORE, STORAGE_S_SOLVE = 0, 1, 2
 
 
 class ParameterError(ValueError):

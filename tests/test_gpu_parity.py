@@ -528,3 +528,41 @@ def test_reconstruct_on_device(p, nx, ny, kappa):
                     den = den + c
                 s = s + num / den
             assert u[g] == s / 4.0, (cx, cy)
+
+
+@pytest.mark.parametrize("p,nx,ny,kappa", [(8, 4, 3, 9.0), (16, 4, 3, 30.0), (22, 3, 3, 60.0), (42, 2, 2, 120.0)])
+def test_stored_s_solve_policy(p, nx, ny, kappa):
+    """HPS_STORAGE_S_SOLVE: condense keeps
+    [S_solve | A_ii^-1 f] per leaf; leaf_solve is one GEMV per leaf (K5s) and agrees with the
+    recompute policy to 1e-10; condense's S_solve output is bitwise the recompute-mode K3 one;
+    reconstruct_full_solution works from the store."""
+    X, Y = P.leaf_coords(nx, ny, p)
+    b = P.crystal_field(0.3 + 0.4 * X, 0.3 + 0.4 * Y)
+    f = np.random.default_rng(5).uniform(-1, 1, X.shape)
+    v = np.random.default_rng(6).uniform(-1, 1, (nx * ny, 4 * (p - 1)))
+    gb = P.boundary_samples(nx, ny, p, lambda x, y: x - y)
+    _, _, na = O.mesh_info(nx, ny, p)
+    ua = np.random.default_rng(7).uniform(-1, 1, na)
+    with G().LeafStage(p, nx, ny, kappa) as st:
+        T0, w0, _, S0 = st.condense(b, f, want_S=True)
+        u0 = st.leaf_solve(b, f, v)
+        r0 = st.reconstruct(ua, gb, b, f)
+    with G().LeafStage(p, nx, ny, kappa, storage=G().STORAGE_S_SOLVE) as st:
+        T1, w1, s1, S1 = st.condense(b, f, want_S=True)
+        u1 = st.leaf_solve(np.zeros_like(b), np.zeros_like(f), v)   # b, f are not read
+        r1 = st.reconstruct(ua, gb, b, f)
+    assert not s1.any()
+    assert np.array_equal(T0, T1) and np.array_equal(w0, w1) and np.array_equal(S0, S1)
+    assert rel_fro(u1.reshape(1, -1), u0.reshape(1, -1))[0] <= 1e-10
+    assert np.linalg.norm(r1 - r0) / np.linalg.norm(r0) <= 1e-10
+
+
+def test_stored_s_solve_budget_and_range():
+    p, nx, ny = 42, 3, 3
+    with pytest.raises(G().ParameterError):
+        G().LeafStage(p, nx, ny, 10.0, storage=G().STORAGE_S_SOLVE, workspace_bytes=8 << 20)
+    b, f = random_leaves(p, 9, seed=3)
+    with G().LeafStage(p, nx, ny, 10.0, storage=G().STORAGE_S_SOLVE) as st:
+        st.condense(b[:4], f[:4])
+        with pytest.raises(G().ParameterError):   # leaves 4.. were not condensed
+            st.leaf_solve(b, f, np.zeros((9, 4 * (p - 1))))

@@ -277,6 +277,11 @@ void hps_host_free(void* ptr);
  * mma.sync.m8n8k4.f64 loop (~0.1 s): the roofline denominator of K2/K3. */
 double hps_gpu_fp64_peak_tflops(int device);
 
+/* The same loop run back to back for `seconds` (<= 0: 3 s), rate of the last third: the
+ * power-limited steady state, the denominator for kernels timed inside a long step (as
+ * MEASURED_PEAKS.json's bf16_tflops_sustained). */
+double hps_gpu_fp64_peak_tflops_sustained(int device, double seconds);
+
 /* Library identity (for load checks). */
 const char* hps_gpu_version(void);
 

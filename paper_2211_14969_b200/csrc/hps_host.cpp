@@ -249,6 +249,7 @@ struct hps_gpu_ctx {
   bool no_stage = false;
   bool no_direct = false;   // debug: D2H copies even for mapped pinned outputs
   DevBuf phase_buf;
+  DevBuf sched;                  // persistent-K2 leaf-claim counter (LuArgs::sched)
   DevBuf field_off, field_cent;   // K0 crystal sampler: node offsets, centres
   DevBuf op_A, op_Dn, op_b, op_f, op_v, op_T, op_w, op_st, op_S, op_u;   // operator-path staging
   DevBuf k4_T, k4_w, k4_g, k4_vals, k4_rhs, k4_list;   // assemble_reduced (host buffers), persistent
@@ -380,6 +381,15 @@ void finish_timing(hps_gpu_ctx* ctx) {
   ctx->timing = t;
 }
 
+// K2 launch with the dynamic leaf schedule: the claim counter is zeroed on the launch stream
+// (the persistent kernel falls back to a static split if the counter cannot be allocated).
+static void launch_k2(hps_gpu_ctx* ctx, hpsg::LuArgs a, int n, cudaStream_t st, int force) {
+  if (ctx->sched.ensure(sizeof(int)) == cudaSuccess &&
+      cudaMemsetAsync(ctx->sched.ptr, 0, sizeof(int), st) == cudaSuccess)
+    a.sched = ctx->sched.as<int>();
+  hpsg::launch_lu_schur(a, n, st, force);
+}
+
 // Device pipeline for one chunk of `n` leaves starting at element e (K1 + K2).
 bool use_small(const hps_gpu_ctx* ctx, bool need_factors) {
   if (ctx->small_env == 0 || need_factors || ctx->phase_timers) return false;
@@ -469,19 +479,20 @@ void enqueue_condense_chunk(hps_gpu_ctx* ctx, int e, int n, const double* d_b, c
   a.lockstep = ctx->lockstep_env == 1 || (ctx->lockstep_env != 0 && hpsg::use_g128(d, ctx->force_cfg));
   a.inject = inj;
   if (ctx->phase_timers) {
-    ctx->phase_buf.ensure(size_t(ctx->chunk) * 16 * sizeof(long long));
-    cudaMemsetAsync(ctx->phase_buf.ptr, 0, size_t(n) * 16 * sizeof(long long), st);
+    ctx->phase_buf.ensure(size_t(ctx->chunk) * hpsg::PHASE_SLOTS * sizeof(long long));
+    cudaMemsetAsync(ctx->phase_buf.ptr, 0, size_t(n) * hpsg::PHASE_SLOTS * sizeof(long long), st);
     a.phase_cycles = ctx->phase_buf.as<long long>();
   }
-  hpsg::launch_lu_schur(a, n, st, ctx->force_cfg);
+  launch_k2(ctx, a, n, st, ctx->force_cfg);
   cudaEventRecord(ctx->timing_event(3 * ci + 2), st);
   if (ctx->phase_timers) {
-    std::vector<long long> h(size_t(n) * 16);
+    constexpr int NS = hpsg::PHASE_SLOTS;
+    std::vector<long long> h(size_t(n) * NS);
     cudaMemcpyAsync(h.data(), ctx->phase_buf.ptr, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, st);
     cudaStreamSynchronize(st);
-    double sum[16] = {0};
+    double sum[NS] = {0};
     for (int i = 0; i < n; ++i)
-      for (int k = 0; k < 16; ++k) sum[k] += double(h[size_t(i) * 16 + k]);
+      for (int k = 0; k < NS; ++k) sum[k] += double(h[size_t(i) * NS + k]);
     std::fprintf(stderr,
                  "[hps phase cycles/leaf] U-part %.3g  L-part %.3g  panel %.3g (strips %.3g [start %.3g "
                  "columns %.3g end %.3g] upd-U %.3g upd-L %.3g)  linv %.3g  trailing %.3g\n",
@@ -489,6 +500,26 @@ void enqueue_condense_chunk(hps_gpu_ctx* ctx, int e, int n, const double* d_b, c
                  (sum[2] + sum[8] + sum[9] + sum[10] + sum[6] + sum[7]) / n,
                  (sum[8] + sum[9] + sum[10]) / n, sum[8] / n, sum[9] / n, sum[10] / n, sum[6] / n,
                  sum[7] / n, sum[3] / n, sum[4] / n);
+    if (sum[16] > 0)
+      std::fprintf(stderr, "[hps leaf totals] cycles/leaf %.4g  ns/leaf %.4g  effective SM clock %.0f MHz\n",
+                   sum[5] / n, sum[16] / n, 1e3 * sum[5] / sum[16]);
+    if (sum[16] > 0) {   // busy time per CTA and per SM (load balance of the persistent grid)
+      std::vector<double> cta(4096, 0.0), sm(512, 0.0);
+      for (int i = 0; i < n; ++i) {
+        cta[size_t(h[size_t(i) * NS + 17]) & 4095] += double(h[size_t(i) * NS + 16]);
+        sm[size_t(h[size_t(i) * NS + 18]) & 511] += double(h[size_t(i) * NS + 16]);
+      }
+      auto stats = [](const std::vector<double>& v, double& mn, double& mean, double& mx) {
+        mn = 1e300; mx = 0; mean = 0; int k = 0;
+        for (double x : v) if (x > 0) { mn = std::min(mn, x); mx = std::max(mx, x); mean += x; ++k; }
+        mean /= std::max(1, k);
+      };
+      double a0, a1, a2, b0, b1, b2;
+      stats(cta, a0, a1, a2);
+      stats(sm, b0, b1, b2);
+      std::fprintf(stderr, "[hps balance] busy ms per CTA min %.2f mean %.2f max %.2f | per SM min %.2f mean %.2f max %.2f\n",
+                   a0 * 1e-6, a1 * 1e-6, a2 * 1e-6, b0 * 1e-6, b1 * 1e-6, b2 * 1e-6);
+    }
     if (sum[11] + sum[12] + sum[13] + sum[14] + sum[15] > 0)
       std::fprintf(stderr,
                    "[hps strip column cycles/leaf] keys+redux %.3g  publish %.3g  barrier %.3g  "
@@ -507,6 +538,11 @@ const char* hps_gpu_version(void) { return "hps_leaf_b200 0.2 (sm_100a, DMMA f64
 double hps_gpu_fp64_peak_tflops(int device) {
   if (cudaSetDevice(device) != cudaSuccess) return 0.0;
   return hpsg::measure_dmma_peak_tflops(device);
+}
+
+double hps_gpu_fp64_peak_tflops_sustained(int device, double seconds) {
+  if (cudaSetDevice(device) != cudaSuccess) return 0.0;
+  return hpsg::measure_dmma_peak_tflops(device, seconds > 0.0 ? seconds : 3.0);
 }
 
 void* hps_host_alloc(size_t bytes) {
@@ -1158,7 +1194,7 @@ static cudaError_t enqueue_leaf_solve_chunk(hps_gpu_ctx* ctx, int c0, int n, con
   cudaEventRecord(ctx->timing_event(3 * slot + 1), st);
   a.d = dsolve;
   // (lock-step measured no faster for the leaf-solve factorisation: 10.63 vs 10.45 ms at C2)
-  hpsg::launch_lu_schur(a, n, st);
+  launch_k2(ctx, a, n, st, 0);
   hpsg::launch_backsolve(dsolve, a.ws, a.perm, d_v, d_u,
                          n, st);
   cudaEventRecord(ctx->timing_event(3 * slot + 2), st);
@@ -1565,7 +1601,7 @@ static int operator_pass(hps_gpu_ctx* ctx, bool solve, int32_t e0, int32_t e1, c
     a.minratio = nullptr;
     a.factor = 1;
     a.lockstep = !solve && hpsg::use_g128(d, ctx->force_cfg);
-    hpsg::launch_lu_schur(a, n, st, ctx->force_cfg);
+    launch_k2(ctx, a, n, st, ctx->force_cfg);
     ctx->tkernels += 3;
     if (solve) {
       hpsg::launch_backsolve(d, a.ws, a.perm, ctx->op_v.as<double>(), ctx->op_u.as<double>(), n, st);

@@ -36,6 +36,7 @@ void launch_write_rhs(const LeafDims& d, int col, const double* D2, const double
                       const double* v, double* ws, int n_leaves, cudaStream_t st);
 
 // K2+K3: blocked LU + triangular solves + Schur GEMM -> T, w, status.
+constexpr int PHASE_SLOTS = 20;   // per-leaf profiling counters (LuArgs::phase_cycles)
 struct LuArgs;
 struct LuArgs {
   LeafDims d;           // geometry; R = ni and ntb = 1 for leaf solves
@@ -48,10 +49,12 @@ struct LuArgs {
   int* status;          // per leaf (factor = 1)
   double* minratio;     // per leaf, nullable
   int factor;           // 1: factor A_ii then trailing columns; 0: trailing columns only
-  long long* phase_cycles = nullptr;  // optional 8 counters per leaf (profiling)
+  long long* phase_cycles = nullptr;  // optional PHASE_SLOTS counters per leaf (profiling)
   int lockstep = 0;                   // factor: lock-step multi-leaf kernel (panels aligned)
   int s_with_load = 0;                // K3: S rows hold n_b + 1 entries, the last = +A_ii^{-1} f_i
   const int* inject = nullptr;         // per leaf, nullable
+  int* sched = nullptr;               // persistent K2: leaf-claim counter, zeroed before the
+                                      // launch (nullptr: static leaf split)
 };
 // Two builds of k2_lu_schur.cu: g256 (8-warp CTAs, R <= 2048) and g128 (4-warp CTAs,
 // R <= 640, more leaves per SM).  K3: S_solve = -A_ii^{-1} A_ib from a factored workspace
@@ -147,8 +150,9 @@ void launch_place(int p, int nx, int ny, int e0, int n, const double* ul, double
 void launch_corners(int p, int nx, int ny, const double* xh, const double* wts, const double* ua, const double* g,
                     double* u, cudaStream_t st);
 
-// FP64 tensor peak probe (k9_fp64_peak.cu): TF/s of a register-only DMMA loop on `device`.
-double measure_dmma_peak_tflops(int device);
+// FP64 tensor peak probe (k9_fp64_peak.cu): TF/s of a register-only DMMA loop on `device`;
+// sustain_s <= 0: burst rate, else the rate after sustain_s seconds of continuous load.
+double measure_dmma_peak_tflops(int device, double sustain_s = 0.0);
 
 // K6: matrix-free residual of the global collocation system (k6_residual.cu): per-leaf
 // [sum r_int^2, sum f_int^2] into part_leaf (2 per leaf), per-edge sum r_flux^2 into

@@ -147,6 +147,7 @@ struct Smem {
   unsigned long long full[NSTAGE];   // stage filled (256 thread arrivals)
   unsigned long long empty[NSTAGE];  // stage consumed (8 warp arrivals)
   unsigned gchunk;                   // running K-chunk counter of this CTA
+  int next_leaf;                     // dynamic leaf schedule (LuArgs::sched)
   alignas(16) double wrow[2][NWARP][8];          // per-warp pivot candidate rows + 1/pivot (double-buffered)
   unsigned long long redk[2][NWARP];
   short perm[MAX_RPAD];              // logical -> physical row
@@ -822,8 +823,11 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf, const Gr
   }
   G.sync();
   double minpiv = INFINITY;  // meaningful on thread 0
-  long long* pc = a.phase_cycles ? a.phase_cycles + (size_t)leaf * 16 : nullptr;
+  long long* pc = a.phase_cycles ? a.phase_cycles + (size_t)leaf * PHASE_SLOTS : nullptr;
   long long t_phase = clock64();
+  const long long t_leaf0 = t_phase;
+  unsigned long long ns_leaf0 = 0;
+  if (pc && G.tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns_leaf0));
 
   const double* M = L.M;
   const int ld = d.ld;
@@ -930,6 +934,16 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf, const Gr
   G.sync();
   for (int i = G.tid; i < d.Rpad; i += NT) perm_g[i] = sm->perm[i];
   if (G.tid == 0) {
+    if (pc) {   // whole-leaf clock64 cycles and globaltimer ns (effective SM clock)
+      unsigned long long ns1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns1));
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      pc[5] += clock64() - t_leaf0;
+      pc[16] += (long long)(ns1 - ns_leaf0);
+      pc[17] = blockIdx.x;
+      pc[18] = smid;
+    }
     const double nrm = a.norms[leaf];
     const double ratio = nrm > 0.0 ? minpiv / nrm : 0.0;
     if (a.minratio) a.minratio[leaf] = ratio;
@@ -953,7 +967,23 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k2_lu_schur_kernel(LuArgs a, 
     sm->gchunk = 0;
   }
   __syncthreads();
-  for (int leaf = blockIdx.x; leaf < n_leaves; leaf += gridDim.x) process_leaf<NSLOT>(a, sm, leaf);
+  // Dynamic schedule (a.sched, zeroed before the launch): after its first leaf a CTA claims the
+  // next unclaimed one.  The two CTAs sharing an SM do not progress at the same rate (one
+  // persistently gets more of the DMMA pipe: 521 vs 693 ms of busy time for 16 leaves each at
+  // C4, profiles/r02_k2_balance.log), so a static leaf split leaves the faster CTA idle for the
+  // last ~12% of the launch.  A leaf's result does not depend on which CTA computes it.
+  int leaf = blockIdx.x;
+  while (leaf < n_leaves) {
+    process_leaf<NSLOT>(a, sm, leaf);
+    if (a.sched) {
+      if (threadIdx.x == 0) sm->next_leaf = (int)gridDim.x + atomicAdd(a.sched, 1);
+      __syncthreads();
+      leaf = sm->next_leaf;
+      __syncthreads();
+    } else {
+      leaf += gridDim.x;
+    }
+  }
 }
 
 // Lock-step multi-leaf kernel: one CTA per SM with CTAS_PER_SM groups of NT threads, each

@@ -68,7 +68,8 @@ EXPORTED = ["hps_gpu_create", "hps_gpu_destroy", "hps_gpu_last_error", "hps_gpu_
             "hps_gpu_multi_ctx", "hps_gpu_multi_condense", "hps_gpu_multi_leaf_solve",
             "hps_gpu_multi_assemble_reduced", "hps_shard_range", "hps_reduced_cut_edges",
             "hps_reduced_host_edges", "hps_gpu_condense_assemble", "hps_gpu_reconstruct",
-            "hps_gpu_reconstruct_device", "hps_gpu_fp64_peak_tflops", "hps_gpu_set_option"]
+            "hps_gpu_reconstruct_device", "hps_gpu_fp64_peak_tflops", "hps_gpu_fp64_peak_tflops_sustained",
+            "hps_gpu_set_option"]
 
 
 def lib():
@@ -83,6 +84,8 @@ def lib():
         L.hps_gpu_version.restype = C.c_char_p
         L.hps_gpu_fp64_peak_tflops.restype = C.c_double
         L.hps_gpu_fp64_peak_tflops.argtypes = [C.c_int]
+        L.hps_gpu_fp64_peak_tflops_sustained.restype = C.c_double
+        L.hps_gpu_fp64_peak_tflops_sustained.argtypes = [C.c_int, C.c_double]
         L.hps_gpu_create.argtypes = [C.c_int, C.POINTER(_Desc), C.POINTER(C.c_void_p)]
         L.hps_gpu_destroy.argtypes = [C.c_void_p]
         L.hps_host_alloc.restype = C.c_void_p
@@ -411,9 +414,12 @@ class LeafStage:
         return rp, ci, vals, rhs
 
 
-def fp64_peak_tflops(device=0):
-    """FP64 tensor (DMMA) peak of the GPU measured now (hps_gpu_fp64_peak_tflops)."""
-    v = lib().hps_gpu_fp64_peak_tflops(device)
+def fp64_peak_tflops(device=0, sustained_s=0.0):
+    """FP64 tensor (DMMA) peak of the GPU measured now: burst (hps_gpu_fp64_peak_tflops) or,
+    with sustained_s > 0, after that many seconds of continuous load
+    (hps_gpu_fp64_peak_tflops_sustained)."""
+    v = (lib().hps_gpu_fp64_peak_tflops_sustained(device, float(sustained_s)) if sustained_s > 0
+         else lib().hps_gpu_fp64_peak_tflops(device))
     if not v > 0:
         raise CudaError("FP64 peak probe failed")
     return v

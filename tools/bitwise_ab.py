@@ -11,7 +11,7 @@ if sys.argv[1] == "--cmp":
     sys.exit(1 if bad else 0)
 from paper_2211_14969_b200 import leaf_gpu as G, problems as P
 out = {}
-for name, n in (("C4", 300), ("C3", 300), ("C2", 700), ("C1", 256)):
+for name, n in (("C4", 300), ("C3", 300), ("C2", 700), ("C1", 128)):
     cfg = P.config(name)
     p = cfg["p"]
     X, Y = P.leaf_coords(cfg["nx"], cfg["ny"], p, elements=np.arange(cfg["n_leaves"] // 2, cfg["n_leaves"] // 2 + n))

@@ -106,19 +106,38 @@ __global__ void __launch_bounds__(256) k5s_apply_kernel(int p, const double* __r
   const int leaf = blockIdx.x;
   const int q = p - 2, ni = q * q, nb = 4 * (p - 1), pp = p * p;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sub = lane >> 3, l8 = lane & 7;   // 4 rows per warp, 8 lanes per row
   const double* Sl = S + (size_t)leaf * ni * (nb + 1);
   const double* vl = v + (size_t)leaf * nb;
   double* ul = u + (size_t)leaf * pp;
-  for (int i = warp; i < ni; i += 8) {
-    const double* row = Sl + (size_t)i * (nb + 1);
-    double acc = 0.0;
-    for (int k = lane; k < nb; k += 32) acc = fma(__ldg(row + k), __ldg(vl + k), acc);
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (lane == 0) ul[interior_local(i, p)] = __dadd_rn(__ldg(row + nb), acc);
-  }
+  __shared__ double vs[4 * 64];   // nb <= 4 (p - 1) <= 256 for p <= 65
   for (int k = threadIdx.x; k < nb; k += 256) {
+    const double x = __ldg(vl + k);
+    vs[k] = x;
     int e;
-    ul[boundary_local(k, p, &e)] = __ldg(vl + k);
+    ul[boundary_local(k, p, &e)] = x;
+  }
+  __syncthreads();
+  // u_i = [S_solve | A_ii^{-1} f]_i . [v ; 1]: 8 lanes stride a row with three independent
+  // partial sums (more loads in flight per warp than one warp per row), then a 3-step
+  // shuffle reduction inside the 8-lane group.
+  for (int b = 4 * warp; b < ni; b += 32) {   // warp-uniform trip count (full-mask shuffles)
+    const int i = b + sub;
+    const bool ok = i < ni;
+    const double* row = Sl + (size_t)(ok ? i : ni - 1) * (nb + 1);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    int k = l8;
+    for (; k + 16 < nb; k += 24) {
+      a0 = fma(__ldcs(row + k), vs[k], a0);
+      a1 = fma(__ldcs(row + k + 8), vs[k + 8], a1);
+      a2 = fma(__ldcs(row + k + 16), vs[k + 16], a2);
+    }
+    for (; k < nb; k += 8) a0 = fma(__ldcs(row + k), vs[k], a0);
+    double acc = (a0 + a1) + a2;
+    acc += __shfl_xor_sync(0xffffffffu, acc, 4);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    if (ok && l8 == 0) ul[interior_local(i, p)] = __dadd_rn(__ldcs(row + nb), acc);
   }
 }
 

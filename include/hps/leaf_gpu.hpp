@@ -49,7 +49,13 @@ class ResonanceError : public std::runtime_error {
 
 namespace hps {
 
-enum class StoragePolicy { Recompute = HPS_STORAGE_RECOMPUTE, Store = HPS_STORAGE_STORE };
+// Recompute (default) re-forms the leaf factors in leaf_solve; Store keeps them;
+// SSolve keeps [S_solve | A_ii^-1 f] so leaf_solve is one GEMV per leaf.
+enum class StoragePolicy {
+  Recompute = HPS_STORAGE_RECOMPUTE,
+  Store = HPS_STORAGE_STORE,
+  SSolve = HPS_STORAGE_S_SOLVE
+};
 
 // MeshParams: unit-size square elements of side a on an
 // nx x ny grid starting at the origin.

@@ -217,6 +217,17 @@ int main() {
     const double rres = stage.relerr_res(u);   // Eq. 7, matrix-free on the GPU (K6)
     std::printf("relerr_res %.3e\n", rres);
     if (!(rres <= 1e-9)) { std::printf("FAIL relerr_res\n"); ++fails; }
+    {  // storage policy SSolve: the same full solution through the kept S_solve blocks
+      hps::b200::LeafStageConfig sc;
+      sc.storage = hps::StoragePolicy::SSolve;
+      hps::b200::LeafStage st2(topo, spec, sc);
+      st2.batched_condense();
+      const auto u2 = st2.reconstruct_full_solution(ua);
+      double dn = 0, dd = 0;
+      for (size_t i = 0; i < u.size(); ++i) { dn += (u2[i] - u[i]) * (u2[i] - u[i]); dd += u[i] * u[i]; }
+      std::printf("storage SSolve vs Recompute full solution: rel %.3e\n", std::sqrt(dn / dd));
+      if (!(std::sqrt(dn / dd) <= 1e-10)) { std::printf("FAIL SSolve policy\n"); ++fails; }
+    }
     try {
       stage.batched_condense(std::vector<double>(5, 0.0));
       std::printf("FAIL no ParameterError for bad f\n");

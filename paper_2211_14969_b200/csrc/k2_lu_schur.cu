@@ -81,6 +81,15 @@ constexpr int NWARP = NT / 32;
 #ifndef HPS_KC
 #define HPS_KC 16
 #endif
+#ifndef HPS_OWNER_SWITCH
+#define HPS_OWNER_SWITCH 1   // pivot-row publish: switch on the slot instead of a select chain
+#endif
+#ifndef HPS_STRIP_REDUX2
+#define HPS_STRIP_REDUX2 1   // cross-warp pivot arg-max with redux.sync on the lanes
+#endif
+#ifndef HPS_STRIP_LEAN
+#define HPS_STRIP_LEAN 1   // candidate carried through the arg-max, key bits fixed per strip
+#endif
 
 // Column offset inside a row of the leaf matrix (row-major).  The tile microbenchmark
 // redefines these to measure a column-blocked layout (tools/microbench/tile_bench.cu).
@@ -492,6 +501,15 @@ __device__ void base_strip(const Grp& G, const LeafCtx& L, int e, int sw, double
       }
     }
   }
+#if HPS_STRIP_LEAN
+  unsigned elig = 0;
+  unsigned klo[NSLOT];
+#pragma unroll
+  for (int s = 0; s < NSLOT; ++s) {
+    if (((active >> s) & 1u) && phys[s] < L.ni) elig |= 1u << s;
+    klo[s] = static_cast<unsigned>(0x7FF - phys[s]);
+  }
+#endif
   G.sync();  // all perm reads done before thread 0 starts swapping
   PHASE_MARK(8);
   int pivrow[4];
@@ -502,6 +520,18 @@ __device__ void base_strip(const Grp& G, const LeafCtx& L, int e, int sw, double
     const int buf = j & 1;
     unsigned long long best = 0ull;
     int bs = 0;
+#if HPS_STRIP_LEAN
+    // The candidate value rides along with the arg-max; eligibility and the low key bits were
+    // fixed when the strip was loaded (elig tracks the pivoted rows).
+    double cand = 0.0;
+#pragma unroll
+    for (int s = 0; s < NSLOT; ++s) {
+      const unsigned long long k = ((elig >> s) & 1u)
+          ? (static_cast<unsigned long long>(__double_as_longlong(x[s][j])) & 0x7FFFFFFFFFFFF800ull) | klo[s]
+          : 0ull;
+      if (k > best) { best = k; bs = s; cand = x[s][j]; }
+    }
+#else
 #pragma unroll
     for (int s = 0; s < NSLOT; ++s) {
       const unsigned long long k =
@@ -514,6 +544,7 @@ __device__ void base_strip(const Grp& G, const LeafCtx& L, int e, int sw, double
 #pragma unroll
     for (int s = 1; s < NSLOT; ++s)
       if (s == bs) cand = x[s][j];
+#endif
     const double rcand = best != 0ull ? fast_rcp(cand) : 0.0;
     // Warp arg-max of the 64-bit keys with two redux.sync (high word, then low word among
     // the lanes holding the maximal high word).
@@ -524,18 +555,44 @@ __device__ void base_strip(const Grp& G, const LeafCtx& L, int e, int sw, double
     STRIP_MARK(11);
     if (lane == 0) L.redk[buf * NWARP + warp] = wbest;
     if (best == wbest && best != 0ull) {  // this lane owns the warp's candidate row
+      double* wr = L.wrow + (buf * NWARP + warp) * 8;
+#if HPS_OWNER_SWITCH
+      // One indirect branch to the slot's two stores instead of a select chain over all slots
+      // (the chain is issued by the whole warp for one active lane).
+      switch (bs) {
+#define HPS_PUB(S)                                                                    \
+  case S:                                                                           \
+    if (S < NSLOT) {                                                                \
+      *reinterpret_cast<double2*>(wr) = make_double2(x[S % NSLOT][0], x[S % NSLOT][1]); \
+      *reinterpret_cast<double2*>(wr + 2) = make_double2(x[S % NSLOT][2], x[S % NSLOT][3]); \
+    }                                                                               \
+    break;
+        HPS_PUB(0) HPS_PUB(1) HPS_PUB(2) HPS_PUB(3) HPS_PUB(4) HPS_PUB(5) HPS_PUB(6) HPS_PUB(7)
+#undef HPS_PUB
+      }
+#else
       double r0 = x[0][0], r1 = x[0][1], r2 = x[0][2], r3 = x[0][3];
 #pragma unroll
       for (int s = 1; s < NSLOT; ++s)
         if (s == bs) { r0 = x[s][0]; r1 = x[s][1]; r2 = x[s][2]; r3 = x[s][3]; }
-      double* wr = L.wrow + (buf * NWARP + warp) * 8;
       *reinterpret_cast<double2*>(wr) = make_double2(r0, r1);
       *reinterpret_cast<double2*>(wr + 2) = make_double2(r2, r3);
+#endif
       wr[4] = rcand;   // dgetf2-style reciprocal 1/pivot
     }
     STRIP_MARK(12);
     G.sync();
     STRIP_MARK(13);
+#if HPS_STRIP_REDUX2
+    // Cross-warp arg-max on the lanes: lane w reads warp w's key, two redux.sync as above, the
+    // winner is the lowest lane holding the maximum (keys are unique per row).
+    const unsigned long long kw = lane < NWARP ? L.redk[buf * NWARP + lane] : 0ull;
+    const unsigned khi = static_cast<unsigned>(kw >> 32);
+    const unsigned kmhi = __reduce_max_sync(0xffffffffu, khi);
+    const unsigned kmlo = __reduce_max_sync(0xffffffffu, khi == kmhi ? static_cast<unsigned>(kw) : 0u);
+    const unsigned long long kb = (static_cast<unsigned long long>(kmhi) << 32) | kmlo;
+    const int ww = __ffs(__ballot_sync(0xffffffffu, lane < NWARP && kw == kb)) - 1;
+#else
     unsigned long long kb = L.redk[buf * NWARP];
     int ww = 0;
 #pragma unroll
@@ -543,6 +600,7 @@ __device__ void base_strip(const Grp& G, const LeafCtx& L, int e, int sw, double
       const unsigned long long k = L.redk[buf * NWARP + w];
       if (k > kb) { kb = k; ww = w; }
     }
+#endif
     const int pphys = 0x7FF - static_cast<int>(kb & 0x7FFull);
     const double* wr = L.wrow + (buf * NWARP + ww) * 8;
     const double2 p01 = *reinterpret_cast<const double2*>(wr);
@@ -554,7 +612,12 @@ __device__ void base_strip(const Grp& G, const LeafCtx& L, int e, int sw, double
     STRIP_MARK(14);
 #pragma unroll
     for (int s = 0; s < NSLOT; ++s) {
-      if (phys[s] == pphys) active &= ~(1u << s);
+      if (phys[s] == pphys) {
+        active &= ~(1u << s);
+#if HPS_STRIP_LEAN
+        elig &= ~(1u << s);
+#endif
+      }
       if ((active >> s) & 1u) {
         const double l = x[s][j] * rpiv;
         x[s][j] = l;

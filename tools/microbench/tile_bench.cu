@@ -13,10 +13,13 @@
 #include "../../paper_2211_14969_b200/csrc/k2_lu_schur.cu"
 
 using namespace hpsg;
-using namespace hpsg::g256;
+using namespace hpsg::HPS_CFG;
 
 template <class TL, bool HOT = false>
-__global__ void __launch_bounds__(NT, 2) tile_bench_kernel(double* ws, int ld, int K, int reps) {
+#ifndef TB_MINB
+#define TB_MINB 2
+#endif
+__global__ void __launch_bounds__(NT, TB_MINB) tile_bench_kernel(double* ws, int ld, int K, int reps) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem* sm = reinterpret_cast<Smem*>(smem_raw);
   for (int i = threadIdx.x; i < MAX_RPAD; i += NT) sm->perm[i] = (short)i;
@@ -131,8 +134,16 @@ int main() {
   run_all_compute();
   const int ld = 2048;
   double* ws;
-  cudaMalloc(&ws, (size_t)296 * 2048 * ld * 8 + (1 << 20));
-  cudaMemset(ws, 0, (size_t)296 * 2048 * ld * 8);
+  cudaMalloc(&ws, (size_t)592 * 2048 * ld * 8 + (1 << 20));
+  cudaMemset(ws, 0, (size_t)592 * 2048 * ld * 8);
+#ifdef TB_G128   // -DHPS_NT=128 -DHPS_CFG=g128 -DHPS_MAX_ROWS=640 -DHPS_NSTAGE=2 -DTB_MINB=4 -DTB_G128
+  for (int ctas : {148, 296, 592}) {
+    run<TileL>("64x64", ctas, 400, 100, ws, ld);
+    run<TileL>("64x64", ctas, 192, 200, ws, ld);
+    run<TileL>("64x64", ctas, 64, 400, ws, ld);
+  }
+  return 0;
+#endif
   for (int ctas : {148, 296}) {
     run<TileL>("128x64", ctas, 1024, 40, ws, ld);
     run<TileU>("64x128", ctas, 1024, 40, ws, ld);

@@ -216,7 +216,26 @@ def test_resonance_error_reports_smallest_element():
             st.leaf_solve(b, f, np.zeros((nx * ny, 4 * (p - 1))))
 
 
+@pytest.mark.parametrize("p,kappa", [(24, 60.0), (25, 60.0), (26, 70.0), (44, 300.0), (45, 300.0)])
+def test_condense_parity_kernel_boundaries(p, kappa):
+    """Leaf sizes at the kernel boundaries: p = 24/25 are the largest leaves of the 4-warp
+    lock-step build (R <= 640), p = 26 the smallest of the 8-warp build, p = 44/45 the largest
+    the 8-warp build accepts (R = 2025 <= 2048 rows, 8 strip rows per thread).  Crystal-like
+    variable b, random f, three leaves against the oracle."""
+    n = 3
+    b, f = random_leaves(p, n, seed=100 + p, lo=0.2, hi=0.7)
+    a = 1.0 / n
+    ref = O.batched_condense(p, a, kappa, b, f)
+    with G().LeafStage(p, n, 1, kappa, a=a) as st:
+        T, w, s = st.condense(b, f)
+    assert not s.any()
+    assert rel_fro(T, ref["T"]).max() <= TOL_T
+    assert rel_fro(w, ref["w"]).max() <= TOL_T
+
+
 def test_parameter_errors():
+    with pytest.raises(G().ParameterError):
+        G().LeafStage(46, 2, 2, 1.0)     # beyond the largest leaf the blocked kernel holds
     with pytest.raises(G().ParameterError):
         G().LeafStage(3, 2, 2, 1.0)
     with pytest.raises(G().ParameterError):

@@ -84,6 +84,9 @@ constexpr int NWARP = NT / 32;
 #ifndef HPS_OWNER_SWITCH
 #define HPS_OWNER_SWITCH 1   // pivot-row publish: switch on the slot instead of a select chain
 #endif
+#ifndef HPS_UPF
+#define HPS_UPF 1   // U-part tile init: 0 prefetch the C tile into L1, 1 none (measured best), 2 prefetch Linv_J rows
+#endif
 #ifndef HPS_STRIP_REDUX2
 #define HPS_STRIP_REDUX2 1   // cross-warp pivot arg-max with redux.sync on the lanes
 #endif
@@ -905,6 +908,9 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf, const Gr
   //   (a) U part of block row J      cols right of J   = Linv_J (A - L[J, 0:c0] U[0:c0, :])
   // The U-part tiles of one block row are independent (no sequential block-row chain), and
   // the Linv_J product is fused into the tile epilogue (shared memory, no HBM round trip).
+#ifdef HPS_EPI_MARKS
+  long long epi_main = 0, epi_tail = 0, lpt_main = 0, lpt_tail = 0, njobs = 0;
+#endif
   for (int J = 0; J < d.nblk; ++J) {
     const int c0 = 64 * J;
     const int w = min(64, d.ni - c0);
@@ -917,10 +923,19 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf, const Gr
         auto arow = lrow(rt);
         auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + c0; };
         // columns c0 + w .. c0 + 63 of the last block are A_ii padding (zero): no DMMA there
+#ifdef HPS_EPI_MARKS
+        const long long tl0 = clock64();
+#endif
         tile_mma<TileL>(G, acc, init, arow, brow, c0, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk,
                         nr, HPS_NACT ? w : 64);
+#ifdef HPS_EPI_MARKS
+        const long long tl1 = clock64();
+#endif
         acc_add<TileL>(acc, crow, nr);
         acc_store<TileL>(acc, crow, nr, 64);
+#ifdef HPS_EPI_MARKS
+        if (G.tid == 0) { lpt_main += tl1 - tl0; lpt_tail += clock64() - tl1; ++njobs; }
+#endif
       }
       __threadfence_block();
       G.sync();
@@ -937,24 +952,50 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf, const Gr
     for (int ct = ct_begin; ct < ct_end; ct += TUN) {
       auto crow = [=](int i) -> double* { return L.M + (size_t)perm[c0 + i] * ld + ct; };
       Acc acc;
+#if HPS_UPF == 0
       auto init = [&](Acc& x) { acc_zero(x); acc_prefetch_l1<TileU>(crow, 64); };
+#elif HPS_UPF == 1
+      auto init = [&](Acc& x) { acc_zero(x); };
+#else
+      // keep Linv_J (32 KB, re-read by every tile of the block row) in L1 instead of the C tile
+      auto init = [&](Acc& x) {
+        acc_zero(x);
+        const int wm_ = (G.tid >> 5) % TileU::WM, ln = threadIdx.x & 31;
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(li + (32 * wm_ + ln) * 64));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(li + (32 * wm_ + ln) * 64 + 16));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(li + (32 * wm_ + ln) * 64 + 32));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(li + (32 * wm_ + ln) * 64 + 48));
+      };
+#endif
       auto arow = lrow(c0);
       auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + ct; };
       // Real (non-padding) columns of this tile: A_ii columns end at ni, the trailing block
       // [A_ib | f] at tb0 + nb + 1; padding columns stay zero without DMMA work.
       const int real_end = ct + TUN > d.tb0 ? d.tb0 + d.nb + 1 : d.ni;
       const int nc = HPS_NACT ? min(TUN, real_end - ct) : TUN;
+#ifdef HPS_EPI_MARKS
+      const long long te0 = clock64();
+#endif
       tile_mma<TileU>(G, acc, init, arow, brow, c0, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk,
                       64, nc);
+#ifdef HPS_EPI_MARKS
+      const long long te1 = clock64();
+#endif
       acc_add<TileU>(acc, crow, 64);
       linv_apply<TRI_LOWER>(G, acc, li, sm->pipe, nc);
       acc_store<TileU>(acc, crow, w, min(TUN, ct_end - ct));
+#ifdef HPS_EPI_MARKS
+      if (G.tid == 0) { epi_main += te1 - te0; epi_tail += clock64() - te1; }
+#endif
     }
     __threadfence_block();
     G.sync();
     PHASE_MARK(0);
   }
 
+#ifdef HPS_EPI_MARKS
+  if (pc && G.tid == 0) { pc[11] += epi_main; pc[12] += epi_tail; pc[13] += lpt_main; pc[14] += lpt_tail; pc[15] += njobs; }
+#endif
   // ---------------- D rows of the trailing columns ----------------
   // T = D_b - L21 U12 ; -w = 0 - L21 (L^{-1} f)      (K = ni)
   for (int tb = 0; tb < d.ntb; ++tb) {

@@ -84,6 +84,12 @@ constexpr int NWARP = NT / 32;
 #ifndef HPS_OWNER_SWITCH
 #define HPS_OWNER_SWITCH 1   // pivot-row publish: switch on the slot instead of a select chain
 #endif
+#ifndef HPS_LPF
+#define HPS_LPF (HPS_NT != 256)   // L-part tile init prefetches the C tile into L1 (measured: helps g128, not g256)
+#endif
+#ifndef HPS_TPF
+#define HPS_TPF 1   // D-row (trailing) tile init prefetches the C tile into L1
+#endif
 #ifndef HPS_UPF
 #define HPS_UPF 1   // U-part tile init: 0 prefetch the C tile into L1, 1 none (measured best), 2 prefetch Linv_J rows
 #endif
@@ -919,7 +925,7 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf, const Gr
         const int nr = min(TLM, d.R - rt);
         auto crow = [=](int i) -> double* { return L.M + (size_t)perm[rt + i] * ld + c0; };
         Acc acc;
-        auto init = [&](Acc& x) { acc_zero(x); acc_prefetch_l1<TileL>(crow, nr); };
+        auto init = [&](Acc& x) { acc_zero(x); if (HPS_LPF) acc_prefetch_l1<TileL>(crow, nr); };
         auto arow = lrow(rt);
         auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + c0; };
         // columns c0 + w .. c0 + 63 of the last block are A_ii padding (zero): no DMMA there
@@ -1006,7 +1012,7 @@ __device__ void process_leaf(const LuArgs& a, Smem* sm, const int leaf, const Gr
       const int nr = min(TLM, d.R - rt);
       auto crow = [=](int i) -> double* { return L.M + (size_t)perm[rt + i] * ld + c0; };
       Acc acc;
-      auto init = [&](Acc& x) { acc_zero(x); acc_prefetch_l1<TileL>(crow, nr); };
+      auto init = [&](Acc& x) { acc_zero(x); if (HPS_TPF) acc_prefetch_l1<TileL>(crow, nr); };
       auto arow = lrow(rt);
       auto brow = [=](int k) -> const double* { return M + (size_t)perm[k] * ld + c0; };
       tile_mma<TileL>(G, acc, init, arow, brow, d.ni, -1.0, sm->pipe, sm->full, sm->empty, &sm->gchunk,
